@@ -1,0 +1,320 @@
+// abi.cu -- the C ABI of include/aqr.h: validation, ownership, launches.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "aqr_internal.cuh"
+
+struct aqr_index {
+  aqr::IndexView v;
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+};
+
+namespace aqr {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+}  // namespace aqr
+
+using aqr::set_error;
+
+namespace {
+
+#define AQR_CHECK_ARG(cond, msg)           \
+  do {                                     \
+    if (!(cond)) {                         \
+      set_error(std::string("aqr: ") + msg); \
+      return AQR_E_INVALID;                \
+    }                                      \
+  } while (0)
+
+aqr_status cuda_fail(cudaError_t e, const char* where) {
+  set_error(std::string("aqr: CUDA error in ") + where + ": " + cudaGetErrorString(e));
+  return (e == cudaErrorMemoryAllocation) ? AQR_E_OOM : AQR_E_CUDA;
+}
+
+#define AQR_CUDA(call, where)                   \
+  do {                                          \
+    cudaError_t e_ = (call);                    \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+int32_t round_up(int32_t x, int32_t m) { return (x + m - 1) / m * m; }
+
+int auto_hbits(int ef) {
+  // visited-hash slots ~ 16 x ef, between 2^10 and 2^13
+  int b = 10;
+  while (b < 13 && (1 << b) < 16 * ef) ++b;
+  return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* aqr_last_error(void) { return aqr::g_err.c_str(); }
+const char* aqr_version(void) { return "aqr-b200 0.1 (sm_100a)"; }
+
+aqr_status aqr_encode(const float* x, int64_t n, int32_t d, int64_t ld_x, const aqr_train_cfg* train,
+                      aqr_quant_params* qp, uint8_t* codes, aqr_stream_t stream) {
+  aqr::g_err.clear();
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  AQR_CHECK_ARG(x != nullptr && codes != nullptr && qp != nullptr, "encode: null pointer");
+  AQR_CHECK_ARG(n >= 1 && d >= 1 && ld_x >= d, "encode: need n >= 1, d >= 1, ld_x >= d");
+  AQR_CHECK_ARG(qp->d == d, "encode: qp->d != d");
+  AQR_CHECK_ARG(qp->d_pad == round_up(d, 16), "encode: qp->d_pad must be round_up(d, 16)");
+  AQR_CHECK_ARG(qp->min_j && qp->max_j && qp->scale_j, "encode: quantizer arrays must be allocated");
+  if (train) {
+    AQR_CHECK_ARG(train->sample_idx != nullptr, "encode: train->sample_idx is null");
+    AQR_CHECK_ARG(train->k_density >= 1 && train->k_density <= 32, "encode: k_density must be in [1, 32]");
+    AQR_CHECK_ARG(train->n_sample > train->k_density && train->n_sample <= n,
+                  "encode: need k_density < n_sample <= n");
+    AQR_CHECK_ARG(train->p_max >= 0.0 && train->p_max <= 50.0, "encode: p_max must be in [0, 50]");
+    AQR_CHECK_ARG(train->eps > 0.0, "encode: eps must be > 0");
+    AQR_CHECK_ARG(std::isnan(train->delta_override) ||
+                      (train->delta_override >= 0.0 && train->delta_override <= 1.0),
+                  "encode: delta_override must be NaN or in [0, 1]");
+    double* meta = nullptr;
+    double* rho = nullptr;
+    void* tmp = nullptr;
+    AQR_CUDA(cudaMallocAsync((void**)&meta, 4 * sizeof(double), s), "encode: alloc");
+    const bool need_rho = std::isnan(train->delta_override) || train->rho_out;
+    if (need_rho) {
+      rho = train->rho_out;
+      if (!rho) AQR_CUDA(cudaMallocAsync((void**)&rho, sizeof(double) * train->n_sample, s), "encode: alloc");
+      AQR_CUDA(aqr::launch_density(x, ld_x, d, train->sample_idx, train->n_sample, train->k_density, train->eps,
+                                   rho, s),
+               "encode: density kernel");
+    }
+    AQR_CUDA(aqr::launch_delta(std::isnan(train->delta_override) ? rho : nullptr, train->n_sample, train->eps,
+                               train->delta_override, train->p_max, meta, s),
+             "encode: delta kernel");
+    AQR_CUDA(cudaMallocAsync(&tmp, sizeof(float) * (size_t)n * d, s), "encode: alloc");
+    AQR_CUDA(aqr::launch_train_columns(x, n, d, ld_x, meta, train->eps, qp->min_j, qp->max_j, qp->scale_j, tmp, s),
+             "encode: percentile kernels");
+    double hmeta[4] = {0, 0, 0, 0};
+    AQR_CUDA(cudaMemcpyAsync(hmeta, meta, 3 * sizeof(double), cudaMemcpyDeviceToHost, s), "encode: copy");
+    AQR_CUDA(cudaFreeAsync(tmp, s), "encode: free");
+    AQR_CUDA(cudaFreeAsync(meta, s), "encode: free");
+    if (need_rho && !train->rho_out) AQR_CUDA(cudaFreeAsync(rho, s), "encode: free");
+    AQR_CUDA(cudaStreamSynchronize(s), "encode: sync");
+    qp->delta = hmeta[0];
+    qp->p_low = hmeta[1];
+    qp->p_high = hmeta[2];
+  }
+  AQR_CUDA(aqr::launch_encode(x, n, d, ld_x, qp->min_j, qp->scale_j, codes, qp->d_pad, s), "encode: pack kernel");
+  return AQR_OK;
+}
+
+aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_stream_t stream) {
+  aqr::g_err.clear();
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  AQR_CHECK_ARG(desc != nullptr && out != nullptr, "upload: null pointer");
+  const aqr_index_desc& D = *desc;
+  AQR_CHECK_ARG(D.n >= 1 && D.n < (int64_t(1) << 31), "upload: need 1 <= n < 2^31");
+  AQR_CHECK_ARG(D.d >= 1, "upload: d >= 1");
+  AQR_CHECK_ARG(D.d_pad == round_up(D.d, 16), "upload: d_pad must be round_up(d, 16)");
+  AQR_CHECK_ARG(D.d_pad <= 2048, "upload: d > 2048 unsupported");
+  AQR_CHECK_ARG(D.metric == AQR_L2 || D.metric == AQR_IP, "upload: bad metric");
+  AQR_CHECK_ARG(D.codes && D.base && D.min_j && D.scale_j && D.adj0 && D.upper_off, "upload: null array");
+  AQR_CHECK_ARG(D.ld_base >= D.d, "upload: ld_base < d");
+  AQR_CHECK_ARG(D.M >= 1 && 2 * D.M <= 1024, "upload: need 1 <= M <= 512");
+  AQR_CHECK_ARG(D.max_level >= 0 && D.max_level <= 64, "upload: bad max_level");
+  AQR_CHECK_ARG(D.entry_point >= 0 && D.entry_point < D.n, "upload: entry_point out of range");
+  AQR_CHECK_ARG(D.upper_rows >= 0 && (D.upper_rows == 0 || D.adj_upper), "upload: adj_upper missing");
+  AQR_CHECK_ARG(D.id_base >= 0 && D.id_base + D.n <= (int64_t(1) << 31), "upload: id_base + n must fit int32");
+  const int64_t n = D.n;
+  const int32_t cap0 = 2 * D.M, M = D.M;
+  // host-side validation of the graph
+  for (int64_t i = 0; i < n * cap0; ++i)
+    AQR_CHECK_ARG(D.adj0[i] >= -1 && D.adj0[i] < n, "upload: adj0 id out of range");
+  std::vector<int32_t> up_off((size_t)n);
+  for (int64_t v = 0; v < n; ++v) {
+    AQR_CHECK_ARG(D.upper_off[v] >= -1 && D.upper_off[v] < D.upper_rows, "upload: upper_off out of range");
+    up_off[v] = (int32_t)D.upper_off[v];
+  }
+  for (int64_t i = 0; i < D.upper_rows * M; ++i)
+    AQR_CHECK_ARG(D.adj_upper[i] >= -1 && D.adj_upper[i] < n, "upload: adj_upper id out of range");
+  if (D.max_level > 0) {
+    AQR_CHECK_ARG(D.upper_off[D.entry_point] >= 0 && D.upper_off[D.entry_point] + D.max_level <= D.upper_rows,
+                  "upload: entry point must have level max_level");
+  }
+  aqr_index* ix = new aqr_index();
+  auto alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes < 16 ? 16 : bytes) != cudaSuccess) return nullptr;
+    ix->allocs.push_back(p);
+    ix->bytes += bytes;
+    return p;
+  };
+  auto fail = [&](aqr_status st) {
+    aqr_index_free(ix);
+    return st;
+  };
+  aqr::IndexView& V = ix->v;
+  V.n = n;
+  V.d = D.d;
+  V.d_pad = D.d_pad;
+  V.d4 = round_up(D.d, 4);
+  V.metric = (int32_t)D.metric;
+  V.id_base = D.id_base;
+  V.M = M;
+  V.cap0 = cap0;
+  V.ld0 = round_up(cap0, 8);
+  V.max_level = D.max_level;
+  V.entry = D.entry_point;
+  uint8_t* codes = (uint8_t*)alloc((size_t)n * D.d_pad);
+  float* base = (float*)alloc(sizeof(float) * (size_t)n * V.d4);
+  float* mn = (float*)alloc(sizeof(float) * V.d4);
+  float* sc = (float*)alloc(sizeof(float) * V.d4);
+  int32_t* a0 = (int32_t*)alloc(sizeof(int32_t) * (size_t)n * V.ld0);
+  int32_t* au = (int32_t*)alloc(sizeof(int32_t) * (size_t)(D.upper_rows > 0 ? D.upper_rows * M : 1));
+  int32_t* uo = (int32_t*)alloc(sizeof(int32_t) * (size_t)n);
+  if (!codes || !base || !mn || !sc || !a0 || !au || !uo) {
+    set_error("aqr: upload: device allocation failed");
+    return fail(AQR_E_OOM);
+  }
+  cudaError_t e = cudaSuccess;
+  auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  chk(cudaMemcpyAsync(codes, D.codes, (size_t)n * D.d_pad, cudaMemcpyDeviceToDevice, s));
+  if (V.d4 != D.d) chk(cudaMemsetAsync(base, 0, sizeof(float) * (size_t)n * V.d4, s));
+  chk(cudaMemcpy2DAsync(base, sizeof(float) * V.d4, D.base, sizeof(float) * D.ld_base, sizeof(float) * D.d, n,
+                        cudaMemcpyDeviceToDevice, s));
+  std::vector<float> ones(V.d4, 1.0f);
+  chk(cudaMemsetAsync(mn, 0, sizeof(float) * V.d4, s));
+  chk(cudaMemcpyAsync(sc, ones.data(), sizeof(float) * V.d4, cudaMemcpyHostToDevice, s));
+  chk(cudaMemcpyAsync(mn, D.min_j, sizeof(float) * D.d, cudaMemcpyDeviceToDevice, s));
+  chk(cudaMemcpyAsync(sc, D.scale_j, sizeof(float) * D.d, cudaMemcpyDeviceToDevice, s));
+  chk(cudaMemsetAsync(a0, 0xff, sizeof(int32_t) * (size_t)n * V.ld0, s));
+  chk(cudaMemcpy2DAsync(a0, sizeof(int32_t) * V.ld0, D.adj0, sizeof(int32_t) * cap0, sizeof(int32_t) * cap0, n,
+                        cudaMemcpyHostToDevice, s));
+  if (D.upper_rows > 0)
+    chk(cudaMemcpyAsync(au, D.adj_upper, sizeof(int32_t) * (size_t)D.upper_rows * M, cudaMemcpyHostToDevice, s));
+  chk(cudaMemcpyAsync(uo, up_off.data(), sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice, s));
+  chk(cudaStreamSynchronize(s));
+  if (e != cudaSuccess) {
+    aqr_status st = cuda_fail(e, "upload");
+    return fail(st);
+  }
+  V.codes = codes;
+  V.base = base;
+  V.min_j = mn;
+  V.scale_j = sc;
+  V.adj0 = a0;
+  V.adj_up = au;
+  V.up_off = uo;
+  *out = ix;
+  return AQR_OK;
+}
+
+void aqr_index_free(aqr_index* ix) {
+  if (!ix) return;
+  for (void* p : ix->allocs) cudaFree(p);
+  delete ix;
+}
+
+size_t aqr_index_device_bytes(const aqr_index* ix) { return ix ? ix->bytes : 0; }
+
+size_t aqr_search_workspace_size(const aqr_index*, int64_t, const aqr_search_params*) { return 256; }
+
+static aqr_status check_search_params(const aqr_search_params* p, bool need_ef) {
+  AQR_CHECK_ARG(p != nullptr, "search: params null");
+  AQR_CHECK_ARG(p->k >= 1 && p->k <= 1024, "search: need 1 <= k <= 1024");
+  if (need_ef) {
+    AQR_CHECK_ARG(p->n_coarse >= p->k, "search: need n_coarse >= k");
+    AQR_CHECK_ARG(p->ef >= p->n_coarse, "search: need ef >= n_coarse");
+    AQR_CHECK_ARG(p->ef <= 4096, "search: ef > 4096 unsupported");
+    AQR_CHECK_ARG(p->n_rerank >= 0 && p->n_rerank <= p->n_coarse, "search: need 0 <= n_rerank <= n_coarse");
+  } else {
+    AQR_CHECK_ARG(p->n_rerank >= 0, "rerank: need n_rerank >= 0");
+  }
+  AQR_CHECK_ARG(p->tau_gap >= 0.0, "search: tau_gap must be >= 0");
+  AQR_CHECK_ARG(p->tau_ratio >= 1.0, "search: tau_ratio must be >= 1");
+  AQR_CHECK_ARG(p->assemble_mode == 0 || p->assemble_mode == 1, "search: assemble_mode must be 0 or 1");
+  AQR_CHECK_ARG(p->visited_bits == 0 || (p->visited_bits >= 6 && p->visited_bits <= 16),
+                "search: visited_bits must be 0 or in [6, 16]");
+  AQR_CHECK_ARG(p->warps_per_block >= 0 && p->warps_per_block <= 8, "search: warps_per_block must be in [0, 8]");
+  return AQR_OK;
+}
+
+static aqr::SearchCfg make_cfg(const aqr_search_params* p) {
+  aqr::SearchCfg c;
+  c.k = p->k;
+  c.ef = p->ef;
+  c.n_coarse = p->n_coarse;
+  c.n_rerank = p->n_rerank;
+  c.tau_gap = p->tau_gap;
+  c.tau_ratio = p->tau_ratio;
+  c.early_term = p->early_term;
+  c.assemble_mode = p->assemble_mode;
+  c.hbits = p->visited_bits ? p->visited_bits : auto_hbits(p->ef);
+  return c;
+}
+
+aqr_status aqr_search(const aqr_index* ix, const float* q, int64_t nq, int64_t ld_q, const aqr_search_params* p,
+                      int32_t* out_ids, float* out_dist, const aqr_debug* debug, void* ws, size_t ws_bytes,
+                      aqr_stream_t stream) {
+  aqr::g_err.clear();
+  AQR_CHECK_ARG(ix != nullptr, "search: index null");
+  aqr_status st = check_search_params(p, true);
+  if (st != AQR_OK) return st;
+  AQR_CHECK_ARG(nq >= 0, "search: nq < 0");
+  if (nq == 0) return AQR_OK;
+  AQR_CHECK_ARG(q && out_ids && out_dist, "search: null pointer");
+  AQR_CHECK_ARG(ld_q >= ix->v.d, "search: ld_q < d");
+  AQR_CHECK_ARG(ws != nullptr && ws_bytes >= 256, "search: workspace too small");
+  AQR_CHECK_ARG(!debug || !debug->exp_ids || debug->exp_cap >= 1, "search: debug exp_cap < 1");
+  aqr::SearchCfg c = make_cfg(p);
+  int wpb = p->warps_per_block ? p->warps_per_block : 4;
+  size_t smem = aqr::search_smem_bytes(ix->v, c, wpb);
+  while (smem > 227 * 1024 && wpb > 1) {
+    --wpb;
+    smem = aqr::search_smem_bytes(ix->v, c, wpb);
+  }
+  if (smem > 227 * 1024) {
+    set_error("aqr: search: per-warp shared memory exceeds 227 KB (reduce ef or visited_bits)");
+    return AQR_E_UNSUPPORTED;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  AQR_CUDA(cudaMemsetAsync(ws, 0, 256, s), "search: memset");
+  AQR_CUDA(aqr::launch_search(ix->v, c, q, nq, ld_q, out_ids, out_dist, debug, static_cast<int*>(ws), wpb, s),
+           "search: kernel launch");
+  return AQR_OK;
+}
+
+aqr_status aqr_rerank(const aqr_index* ix, const float* q, int64_t nq, int64_t ld_q, const int32_t* cand_ids,
+                      int32_t n_cand, const aqr_search_params* p, int32_t* out_ids, float* out_dist,
+                      aqr_stream_t stream) {
+  aqr::g_err.clear();
+  AQR_CHECK_ARG(ix != nullptr, "rerank: index null");
+  aqr_status st = check_search_params(p, false);
+  if (st != AQR_OK) return st;
+  AQR_CHECK_ARG(nq >= 0 && n_cand >= 1 && n_cand <= 4096, "rerank: need nq >= 0, 1 <= n_cand <= 4096");
+  if (nq == 0) return AQR_OK;
+  AQR_CHECK_ARG(q && cand_ids && out_ids && out_dist, "rerank: null pointer");
+  AQR_CHECK_ARG(ld_q >= ix->v.d, "rerank: ld_q < d");
+  aqr::SearchCfg c = make_cfg(p);
+  c.n_coarse = n_cand;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  AQR_CUDA(aqr::launch_rerank(ix->v, c, q, nq, ld_q, cand_ids, n_cand, out_ids, out_dist, s),
+           "rerank: kernel launch");
+  return AQR_OK;
+}
+
+aqr_status aqr_merge_topk(const float* dist, const int32_t* ids, int32_t n_lists, int64_t nq, int32_t k,
+                          float* out_dist, int32_t* out_ids, aqr_stream_t stream) {
+  aqr::g_err.clear();
+  AQR_CHECK_ARG(n_lists >= 1 && n_lists <= 32, "merge: need 1 <= n_lists <= 32");
+  AQR_CHECK_ARG(k >= 1 && nq >= 0, "merge: need k >= 1, nq >= 0");
+  if (nq == 0) return AQR_OK;
+  AQR_CHECK_ARG(dist && ids && out_dist && out_ids, "merge: null pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  AQR_CUDA(aqr::launch_merge(dist, ids, n_lists, nq, k, out_dist, out_ids, s), "merge: kernel launch");
+  return AQR_OK;
+}
+
+}  // extern "C"

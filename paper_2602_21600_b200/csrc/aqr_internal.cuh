@@ -1,0 +1,57 @@
+// aqr_internal.cuh -- shared declarations of the sm_100a implementation of include/aqr.h.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/aqr.h"
+
+namespace aqr {
+
+// Device-side view of an uploaded index (passed by value to kernels).
+struct IndexView {
+  int64_t n;
+  int32_t d, d_pad, d4, metric;
+  int64_t id_base;
+  const uint8_t* codes;   // [n x d_pad]
+  const float* base;      // [n x d4]   (d4 = round_up(d, 4), zero padded)
+  const float* min_j;     // [d4]       (padding: 0)
+  const float* scale_j;   // [d4]       (padding: 1)
+  int32_t M, cap0, ld0;   // layer-0 rows: cap0 = 2M valid entries, stride ld0 (multiple of 8)
+  const int32_t* adj0;    // [n x ld0]
+  const int32_t* adj_up;  // [upper_rows x M]
+  const int32_t* up_off;  // [n] (-1 for level-0 nodes)
+  int32_t max_level, entry;
+};
+
+struct SearchCfg {
+  int32_t k, ef, n_coarse, n_rerank;
+  double tau_gap, tau_ratio;
+  int32_t early_term, assemble_mode;
+  int32_t hbits;          // visited hash slots = 1 << hbits
+};
+
+void set_error(const std::string& msg);
+
+// launchers (defined in encode.cu / search.cu / merge.cu); return cudaError_t of the launch
+cudaError_t launch_density(const float* x, int64_t ld_x, int32_t d, const int32_t* sample, int32_t ns,
+                           int32_t k, double eps, double* rho, cudaStream_t s);
+cudaError_t launch_delta(const double* rho, int32_t ns, double eps, double delta_override, double p_max,
+                         double* meta /*device [3]*/, cudaStream_t s);
+cudaError_t launch_train_columns(const float* x, int64_t n, int32_t d, int64_t ld_x, const double* meta,
+                                 double eps, float* min_j, float* max_j, float* scale_j, void* tmp,
+                                 cudaStream_t s);
+cudaError_t launch_encode(const float* x, int64_t n, int32_t d, int64_t ld_x, const float* min_j,
+                          const float* scale_j, uint8_t* codes, int32_t d_pad, cudaStream_t s);
+cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
+                          int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter,
+                          int warps_per_block, cudaStream_t s);
+cudaError_t launch_rerank(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
+                          const int32_t* cand, int32_t n_cand, int32_t* out_ids, float* out_dist,
+                          cudaStream_t s);
+cudaError_t launch_merge(const float* dist, const int32_t* ids, int32_t n_lists, int64_t nq, int32_t k,
+                         float* out_dist, int32_t* out_ids, cudaStream_t s);
+size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int warps_per_block);
+
+}  // namespace aqr

@@ -1,0 +1,684 @@
+// search.cu -- fused AQR-HNSW query search on sm_100a (aqr_search / aqr_rerank).
+//
+// One warp per query, persistent grid (atomic query counter).  Per query, all inside the
+// kernel (Alg2):
+//   1. quantize the query (Alg2 l.4) into shared memory;
+//   2. greedy descent through layers max_level..1 on d^q (R8);
+//   3. layer-0 beam with ef on d^q (Alg2 l.6-7), "flag form" (R8): W is a sorted
+//      list of <= ef 64-bit keys (d^q << 32 | id << 1 | expanded) in shared memory; each step
+//      expands the smallest unexpanded entry, gathers its adjacency row, tests a visited
+//      hash in shared memory, gathers the unvisited codes with 16-byte loads (LPR lanes per
+//      code row), scores them with dp4a in int32, filters against max W and merges the
+//      survivors with a rank-based parallel merge;
+//   4. Stage 2: decode + asymmetric fp32 distance for C = W[0:N_c] (Alg2 l.8-13);
+//   5. early termination (Alg2 l.15-16, fp64 test on fp32 values, R11);
+//   6. Stage 3: exact fp32 distance over the retained fp32 rows (Alg2 l.18-22, FMA P:197);
+//   7. assembly + top-k (Alg2 l.23-24; fill reading R10 or union S:515) and the store.
+//
+// The path is a gather (pointer chasing), not a contraction: no tensor cores (north_star).
+// Integer results (codes, d^q, W, visit order, ids) are bit-exact with the oracle; fp32
+// sums use a lane-strided FMA order and agree with the oracle's sequential order within
+// 1e-5 relative (north_star tolerance).
+#include <cfloat>
+#include <climits>
+
+#include "aqr_internal.cuh"
+
+namespace aqr {
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kEmpty = 0xffffffffu;
+constexpr int kProbes = 8;
+
+// ------------------------------------------------------------------------------------
+// small helpers
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t qkey(uint32_t d, int32_t id) {
+  return ((uint64_t)d << 32) | ((uint64_t)(uint32_t)id << 1);
+}
+__device__ __forceinline__ int32_t qkey_id(uint64_t k) { return (int32_t)((uint32_t)k >> 1); }
+__device__ __forceinline__ uint32_t qkey_d(uint64_t k) { return (uint32_t)(k >> 32); }
+
+__device__ __forceinline__ uint32_t fkey(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k ^ 0x80000000u) : ~k);
+}
+__device__ __forceinline__ uint64_t akey(float d, int32_t id) {
+  return ((uint64_t)fkey(d) << 32) | (uint32_t)id;
+}
+
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+  uint32_t lo = __shfl_sync(kFull, (uint32_t)v, src), hi = __shfl_sync(kFull, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  uint32_t lo = __shfl_xor_sync(kFull, (uint32_t)v, m), hi = __shfl_xor_sync(kFull, (uint32_t)(v >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) {
+    uint64_t o = shfl_xor_u64(v, m);
+    v = o < v ? o : v;
+  }
+  return v;
+}
+
+// streaming 16-byte gather: read-only path, no L1 allocation (codes are touched once per query)
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// number of keys in sorted a[0:n) strictly less than key
+__device__ __forceinline__ int lower_bound_u64(const uint64_t* a, int n, uint64_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+// same, ignoring the expanded flag bit of W entries
+__device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if ((a[mid] & ~1ull) < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------------------------------
+// per-warp shared-memory layout
+// ------------------------------------------------------------------------------------
+struct Layout {
+  int o_qc, o_qf, o_w, o_h, o_nb, o_nd, o_cand, o_cs, per_warp;
+  int region;  // bytes of the hash region (reused by Stage 2/3)
+};
+
+__host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
+
+Layout make_layout(const IndexView& ix, const SearchCfg& c) {
+  Layout L;
+  int o = 0;
+  L.o_qc = o; o += al16(ix.d_pad);
+  L.o_qf = o; o += al16(4 * ix.d4);
+  L.o_w = o; o += al16(8 * (c.ef + 1));
+  int hb = 4 << c.hbits;
+  int s23 = 20 * c.n_coarse + 32;
+  L.region = hb > s23 ? hb : s23;
+  L.o_h = o; o += al16(L.region);
+  L.o_nb = o; o += al16(4 * ix.ld0);
+  L.o_nd = o; o += al16(4 * ix.ld0);
+  L.o_cand = o; o += al16(8 * ix.ld0);
+  L.o_cs = o; o += al16(8 * ix.ld0);
+  L.per_warp = o;
+  return L;
+}
+
+// ------------------------------------------------------------------------------------
+// d^q for a list of node ids: LPR lanes per code row, CPL 16-byte chunks per lane
+// d^q = sum q^2 + sum x^2 - 2 sum q x  (exact int32; dp4a on u8x4 words)
+// ------------------------------------------------------------------------------------
+template <int LPR, int CPL>
+__device__ __forceinline__ void list_dists(const IndexView& ix, const uint4 (&qreg)[CPL], int qq,
+                                           const int32_t* ids, int m, int32_t* out, int lane) {
+  constexpr int G = 32 / LPR;
+  constexpr int U = CPL == 1 ? 8 : (CPL == 2 ? 4 : 2);
+  const int g = lane / LPR, sub = lane % LPR;
+  const int nch = ix.d_pad >> 4;
+  for (int r0 = 0; r0 < m; r0 += G * U) {
+    uint4 buf[U][CPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = r0 + u * G + g;
+      const int id = r < m ? ids[r] : -1;
+      const uint4* row = reinterpret_cast<const uint4*>(ix.codes + (int64_t)(id < 0 ? 0 : id) * ix.d_pad);
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) {
+        const int c = sub + LPR * t;
+        buf[u][t] = (id >= 0 && c < nch) ? ldg_stream(row + c) : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      unsigned xx = 0, qx = 0;
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) {
+        const uint4 w = buf[u][t], qw = qreg[t];
+        xx = __dp4a(w.x, w.x, xx); qx = __dp4a(qw.x, w.x, qx);
+        xx = __dp4a(w.y, w.y, xx); qx = __dp4a(qw.y, w.y, qx);
+        xx = __dp4a(w.z, w.z, xx); qx = __dp4a(qw.z, w.z, qx);
+        xx = __dp4a(w.w, w.w, xx); qx = __dp4a(qw.w, w.w, qx);
+      }
+      int s = (int)xx - 2 * (int)qx;
+#pragma unroll
+      for (int off = LPR / 2; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+      const int r = r0 + u * G + g;
+      if (sub == 0 && r < m) out[r] = qq + s;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// visited set: open-addressing hash of node ids in shared memory.  A full probe window
+// reports "not visited" without inserting: a false negative only causes a re-evaluation,
+// which the W dedupe absorbs (R15).  False positives cannot occur.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ bool visit_new(uint32_t* h, int hbits, int32_t u, int& fails) {
+  const uint32_t hmask = (1u << hbits) - 1u;
+  uint32_t s = ((uint32_t)u * 2654435761u) >> (32 - hbits);
+#pragma unroll 1
+  for (int p = 0; p < kProbes; ++p) {
+    uint32_t old = atomicCAS(h + s, kEmpty, (uint32_t)u);
+    if (old == kEmpty) return true;
+    if (old == (uint32_t)u) return false;
+    s = (s + 1) & hmask;
+  }
+  ++fails;
+  return true;
+}
+
+// gather row entries >= 0 of a -1 padded adjacency row into nb[] (compacted, order kept);
+// if `h` is non-null, only ids newly inserted in the visited hash are kept.
+__device__ __forceinline__ int gather_row(const int32_t* row, int cap, int32_t* nb, uint32_t* h, int hbits,
+                                          int& fails, int& deg, int lane) {
+  int m = 0;
+  deg = 0;
+  for (int t0 = 0; t0 < cap; t0 += 32) {
+    const int j = t0 + lane;
+    const int32_t u = j < cap ? __ldg(row + j) : -1;
+    deg += __popc(__ballot_sync(kFull, u >= 0));
+    bool keep = u >= 0;
+    if (keep && h) keep = visit_new(h, hbits, u, fails);
+    const uint32_t mask = __ballot_sync(kFull, keep);
+    if (keep) nb[m + __popc(mask & ((1u << lane) - 1u))] = u;
+    m += __popc(mask);
+  }
+  __syncwarp();
+  return m;
+}
+
+// rank sort of n 64-bit distinct keys: dst[rank(src[i])] = src[i]
+__device__ __forceinline__ void rank_sort(const uint64_t* src, uint64_t* dst, int n, int lane) {
+  for (int i = lane; i < n; i += 32) {
+    const uint64_t k = src[i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) r += src[j] < k;
+    dst[r] = k;
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------------------------
+// fp32 distance of the query (smem, zero padded to d4) against one row, lanes own 4-wide
+// chunks c = lane + 32 t; FMA per term; butterfly sum.  Stage 2 decodes the codes
+// (x~ = xhat / scale + min, Alg2 l.11) and Stage 3 reads the fp32 row.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ float warp_sum(float a) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) a = __fadd_rn(a, __shfl_xor_sync(kFull, a, off));
+  return a;
+}
+
+__device__ __forceinline__ float asym_row(const IndexView& ix, const float* qf, int32_t id, int lane) {
+  const uint8_t* crow = ix.codes + (int64_t)id * ix.d_pad;
+  const int n4 = ix.d4 >> 2;
+  float acc = 0.0f;
+  for (int c = lane; c < n4; c += 32) {
+    const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(crow) + c);
+    const float4 qv = reinterpret_cast<const float4*>(qf)[c];
+    const float4 sv = __ldg(reinterpret_cast<const float4*>(ix.scale_j) + c);
+    const float4 mv = __ldg(reinterpret_cast<const float4*>(ix.min_j) + c);
+    const float x0 = __fadd_rn(__fdiv_rn((float)(w & 255u), sv.x), mv.x);
+    const float x1 = __fadd_rn(__fdiv_rn((float)((w >> 8) & 255u), sv.y), mv.y);
+    const float x2 = __fadd_rn(__fdiv_rn((float)((w >> 16) & 255u), sv.z), mv.z);
+    const float x3 = __fadd_rn(__fdiv_rn((float)(w >> 24), sv.w), mv.w);
+    if (ix.metric == 0) {
+      float e;
+      e = __fsub_rn(qv.x, x0); acc = __fmaf_rn(e, e, acc);
+      e = __fsub_rn(qv.y, x1); acc = __fmaf_rn(e, e, acc);
+      e = __fsub_rn(qv.z, x2); acc = __fmaf_rn(e, e, acc);
+      e = __fsub_rn(qv.w, x3); acc = __fmaf_rn(e, e, acc);
+    } else {
+      acc = __fmaf_rn(qv.x, x0, acc);
+      acc = __fmaf_rn(qv.y, x1, acc);
+      acc = __fmaf_rn(qv.z, x2, acc);
+      acc = __fmaf_rn(qv.w, x3, acc);
+    }
+  }
+  acc = warp_sum(acc);
+  return ix.metric == 0 ? acc : __fsub_rn(1.0f, acc);
+}
+
+__device__ __forceinline__ float exact_row(const IndexView& ix, const float* qf, int32_t id, int lane) {
+  const float4* xrow = reinterpret_cast<const float4*>(ix.base + (int64_t)id * ix.d4);
+  const int n4 = ix.d4 >> 2;
+  float acc = 0.0f;
+  for (int c = lane; c < n4; c += 32) {
+    const float4 xv = __ldg(xrow + c);
+    const float4 qv = reinterpret_cast<const float4*>(qf)[c];
+    if (ix.metric == 0) {
+      float e;
+      e = __fsub_rn(qv.x, xv.x); acc = __fmaf_rn(e, e, acc);
+      e = __fsub_rn(qv.y, xv.y); acc = __fmaf_rn(e, e, acc);
+      e = __fsub_rn(qv.z, xv.z); acc = __fmaf_rn(e, e, acc);
+      e = __fsub_rn(qv.w, xv.w); acc = __fmaf_rn(e, e, acc);
+    } else {
+      acc = __fmaf_rn(qv.x, xv.x, acc);
+      acc = __fmaf_rn(qv.y, xv.y, acc);
+      acc = __fmaf_rn(qv.z, xv.z, acc);
+      acc = __fmaf_rn(qv.w, xv.w, acc);
+    }
+  }
+  acc = warp_sum(acc);
+  return ix.metric == 0 ? acc : __fsub_rn(1.0f, acc);
+}
+
+// ------------------------------------------------------------------------------------
+// Stages 2 / ET / 3 / assembly for one query (Alg2 l.8-24).  cid[0:nc] in smem holds C in
+// (d^q, id) order; region holds >= 20*nc bytes of scratch after cid.
+// ------------------------------------------------------------------------------------
+__device__ void finish_query(const IndexView& ix, const SearchCfg& c, const float* qf, int32_t* cid, int nc,
+                             uint64_t* akeys, uint64_t* rkeys, int64_t qi, int32_t* out_ids, float* out_dist,
+                             const aqr_debug& dbg, bool has_dbg, int lane, int64_t* cnt) {
+  // Stage 2: d^a for every entry of C (Alg2 l.10-12)
+  for (int i = 0; i < nc; ++i) {
+    const int32_t id = cid[i];
+    const float da = asym_row(ix, qf, id, lane);
+    if (lane == 0) rkeys[i] = akey(da, id);
+  }
+  __syncwarp();
+  // A <- sort by (d^a, id) (Alg2 l.13)
+  rank_sort(rkeys, akeys, nc, lane);
+  // early termination (Alg2 l.15-16): fp64 test on the fp32 values (R11)
+  const int k = c.k;
+  int term = 0;
+  if (c.early_term && nc > k) {
+    const double ak = (double)fkey_inv((uint32_t)(akeys[k - 1] >> 32));
+    const double ak1 = (double)fkey_inv((uint32_t)(akeys[k] >> 32));
+    const double gap = __ddiv_rn(__dsub_rn(ak1, ak), __dadd_rn(ak, 1e-6));
+    const double ratio = __ddiv_rn(ak1, __dadd_rn(ak, 1e-6));
+    term = (gap > c.tau_gap) || (ratio > c.tau_ratio);
+  }
+  int depth = c.n_rerank < nc ? c.n_rerank : nc;
+  if (term && depth > k) depth = k;
+  // Stage 3: exact distances for A[0:depth] (Alg2 l.19-22)
+  for (int i = 0; i < depth; ++i) {
+    const int32_t id = (int32_t)(uint32_t)akeys[i];
+    const float de = exact_row(ix, qf, id, lane);
+    if (lane == 0) {
+      rkeys[i] = akey(de, id);
+      if (has_dbg && dbg.exact_d) dbg.exact_d[qi * c.n_coarse + i] = de;
+    }
+  }
+  // assembly (Alg2 l.23-24): R = R_exact U (fill: as needed for k / union: the rest of A)
+  int nr = depth;
+  const int extra_end = c.assemble_mode == 0 ? (nc < k ? nc : k) : nc;
+  for (int i = depth + lane; i < extra_end; i += 32) rkeys[i] = akeys[i];
+  if (extra_end > nr) nr = extra_end;
+  __syncwarp();
+  if (has_dbg) {
+    for (int i = lane; i < nc; i += 32) {
+      if (dbg.asym_ids) dbg.asym_ids[qi * c.n_coarse + i] = (int32_t)(uint32_t)akeys[i];
+      if (dbg.asym_d) dbg.asym_d[qi * c.n_coarse + i] = fkey_inv((uint32_t)(akeys[i] >> 32));
+    }
+  }
+  __syncwarp();
+  // sort R by (dist, id) into akeys (A no longer needed) and emit the top k
+  rank_sort(rkeys, akeys, nr, lane);
+  for (int t = lane; t < k; t += 32) {
+    int32_t oid = -1;
+    float od = INFINITY;
+    if (t < nr) {
+      oid = (int32_t)((int64_t)(int32_t)(uint32_t)akeys[t] + ix.id_base);
+      od = fkey_inv((uint32_t)(akeys[t] >> 32));
+    }
+    out_ids[qi * k + t] = oid;
+    out_dist[qi * k + t] = od;
+  }
+  if (lane == 0 && cnt) {
+    cnt[6] = nc;
+    cnt[7] = depth;
+    cnt[8] = term;
+    cnt[9] = nc;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void load_query(const IndexView& ix, const float* q, int64_t ld_q, int64_t qi, float* qf,
+                                           uint8_t* qc, int lane) {
+  const float* qrow = q + qi * ld_q;
+  for (int j = lane; j < ix.d4; j += 32) qf[j] = j < ix.d ? qrow[j] : 0.0f;
+  __syncwarp();
+  if (qc) {
+    // Alg2 l.4: the same quantizer as the base vectors
+    for (int j = lane; j < ix.d_pad; j += 32) {
+      uint32_t code = 0;
+      if (j < ix.d) {
+        const float t = __fsub_rn(qf[j], __ldg(ix.min_j + j));
+        const float u = __fmul_rn(t, __ldg(ix.scale_j + j));
+        code = (uint32_t)roundf(fminf(fmaxf(u, 0.0f), 255.0f));
+      }
+      qc[j] = (uint8_t)code;
+    }
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------------------------
+// the fused search kernel
+// ------------------------------------------------------------------------------------
+template <int LPR, int CPL>
+__global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, Layout L, const float* __restrict__ q,
+                                                     int64_t nq, int64_t ld_q, int32_t* __restrict__ out_ids,
+                                                     float* __restrict__ out_dist, aqr_debug dbg, int has_dbg,
+                                                     int* __restrict__ counter) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  uint8_t* wb = smem + (threadIdx.x >> 5) * L.per_warp;
+  uint8_t* qc = wb + L.o_qc;
+  float* qf = reinterpret_cast<float*>(wb + L.o_qf);
+  uint64_t* W = reinterpret_cast<uint64_t*>(wb + L.o_w);
+  uint32_t* hash = reinterpret_cast<uint32_t*>(wb + L.o_h);
+  int32_t* nb = reinterpret_cast<int32_t*>(wb + L.o_nb);
+  int32_t* nd = reinterpret_cast<int32_t*>(wb + L.o_nd);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(wb + L.o_cand);
+  uint64_t* cs = reinterpret_cast<uint64_t*>(wb + L.o_cs);
+  const int sub = lane % LPR;
+  const int nch = ix.d_pad >> 4;
+  const int ef = c.ef;
+
+  for (;;) {
+    int64_t qi = 0;
+    if (lane == 0) qi = atomicAdd(counter, 1);
+    qi = __shfl_sync(kFull, qi, 0);
+    if (qi >= nq) break;
+    int64_t cnt[AQR_NCOUNT];
+#pragma unroll
+    for (int t = 0; t < AQR_NCOUNT; ++t) cnt[t] = 0;
+    int fails = 0;
+
+    // 1. quantize the query
+    load_query(ix, q, ld_q, qi, qf, qc, lane);
+    uint4 qreg[CPL];
+#pragma unroll
+    for (int t = 0; t < CPL; ++t) {
+      const int ch = sub + LPR * t;
+      qreg[t] = ch < nch ? reinterpret_cast<const uint4*>(qc)[ch] : make_uint4(0, 0, 0, 0);
+    }
+    int qq = 0;
+    for (int j = lane; j < ix.d_pad; j += 32) qq += (int)qc[j] * (int)qc[j];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) qq += __shfl_xor_sync(kFull, qq, off);
+
+    // 2. greedy descent through the upper layers (R8)
+    int32_t cur = ix.entry;
+    if (lane == 0) nb[0] = cur;
+    __syncwarp();
+    list_dists<LPR, CPL>(ix, qreg, qq, nb, 1, nd, lane);
+    __syncwarp();
+    uint32_t dcur = (uint32_t)nd[0];
+    cnt[5] += 1;
+    for (int lv = ix.max_level; lv >= 1; --lv) {
+      for (;;) {
+        __syncwarp();
+        const int32_t* row = ix.adj_up + (int64_t)(__ldg(ix.up_off + cur) + lv - 1) * ix.M;
+        int deg;
+        const int m = gather_row(row, ix.M, nb, nullptr, 0, fails, deg, lane);
+        list_dists<LPR, CPL>(ix, qreg, qq, nb, m, nd, lane);
+        __syncwarp();
+        uint64_t best = qkey(dcur, cur);
+        for (int r = lane; r < m; r += 32) {
+          const uint64_t kk = qkey((uint32_t)nd[r], nb[r]);
+          best = kk < best ? kk : best;
+        }
+        best = warp_min_u64(best);
+        cnt[3] += 1;
+        cnt[4] += deg;
+        cnt[5] += m;
+        if (qkey_id(best) == cur) break;
+        cur = qkey_id(best);
+        dcur = qkey_d(best);
+      }
+    }
+
+    // 3. layer-0 beam (flag form)
+    {
+      uint4* h4 = reinterpret_cast<uint4*>(hash);
+      const int nh4 = (1 << c.hbits) >> 2;
+      for (int t = lane; t < nh4; t += 32) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      W[0] = qkey(dcur, cur);
+      visit_new(hash, c.hbits, cur, fails);
+    }
+    __syncwarp();
+    int size = 1, cursor = 0, nexp = 0;
+    for (;;) {
+      // smallest unexpanded entry of W
+      int pos = -1;
+      for (int b = cursor; b < size; b += 32) {
+        const int i = b + lane;
+        const bool un = i < size && !(W[i] & 1ull);
+        const uint32_t mk = __ballot_sync(kFull, un);
+        if (mk) { pos = b + __ffs(mk) - 1; break; }
+      }
+      if (pos < 0) break;
+      const uint64_t wk = W[pos];
+      const int32_t cnode = qkey_id(wk);
+      __syncwarp();
+      if (lane == 0) {
+        W[pos] = wk | 1ull;
+        if (has_dbg && dbg.exp_ids && nexp < dbg.exp_cap) dbg.exp_ids[qi * dbg.exp_cap + nexp] = cnode;
+      }
+      ++nexp;
+      // neighbours not yet visited
+      int deg;
+      const int m = gather_row(ix.adj0 + (int64_t)cnode * ix.ld0, ix.cap0, nb, hash, c.hbits, fails, deg, lane);
+      cnt[1] += deg;
+      cnt[2] += m;
+      list_dists<LPR, CPL>(ix, qreg, qq, nb, m, nd, lane);
+      __syncwarp();
+      // filter against max W (when full) and drop re-evaluations already in W
+      const uint64_t maxk = size >= ef ? (W[size - 1] & ~1ull) : ~0ull;
+      int np = 0;
+      for (int r0 = 0; r0 < m; r0 += 32) {
+        const int r = r0 + lane;
+        bool ok = false;
+        uint64_t kk = 0;
+        if (r < m) {
+          kk = qkey((uint32_t)nd[r], nb[r]);
+          ok = kk < maxk;
+          if (ok) {
+            const int lb = lower_bound_w(W, size, kk);
+            ok = !(lb < size && (W[lb] & ~1ull) == kk);
+          }
+        }
+        const uint32_t mk = __ballot_sync(kFull, ok);
+        if (ok) cand[np + __popc(mk & ((1u << lane) - 1u))] = kk;
+        np += __popc(mk);
+      }
+      __syncwarp();
+      if (np == 0) {
+        cursor = pos + 1;
+        continue;
+      }
+      // merge: candidate final slot = (#W keys below) + (rank among candidates)
+      rank_sort(cand, cs, np, lane);
+      int first_ins = size;
+      for (int i = lane; i < np; i += 32) {
+        const int lb = lower_bound_w(W, size, cs[i]);
+        nd[i] = lb + i;  // nd reused as the candidate destinations
+        if (i == 0) first_ins = lb;
+      }
+      first_ins = __shfl_sync(kFull, first_ins, 0);
+      __syncwarp();
+      // shift the old entries W[first_ins:size) right, top chunk first (in place)
+      for (int hi = size; hi > first_ins; hi -= 32) {
+        const int lo = hi - 32 > first_ins ? hi - 32 : first_ins;
+        const int i = lo + lane;
+        uint64_t v = 0;
+        int dst = INT_MAX;
+        if (i < hi) {
+          v = W[i];
+          dst = i + lower_bound_u64(cs, np, v & ~1ull);
+        }
+        __syncwarp();
+        if (i < hi && dst < ef) W[dst] = v;
+        __syncwarp();
+      }
+      for (int i = lane; i < np; i += 32)
+        if (nd[i] < ef) W[nd[i]] = cs[i];
+      __syncwarp();
+      size = size + np < ef ? size + np : ef;
+      cursor = first_ins < pos + 1 ? first_ins : pos + 1;
+    }
+    cnt[0] = nexp;
+    cnt[10] = fails;
+
+    // debug: C with d^q
+    const int nc = c.n_coarse < size ? c.n_coarse : size;
+    int32_t* cid = reinterpret_cast<int32_t*>(hash);
+    uint64_t* akeys = reinterpret_cast<uint64_t*>(wb + L.o_h + al16(4 * nc));
+    uint64_t* rkeys = akeys + nc;
+    __syncwarp();
+    for (int i = lane; i < nc; i += 32) {
+      const uint64_t wkk = W[i];
+      cid[i] = qkey_id(wkk);
+      if (has_dbg) {
+        if (dbg.coarse_ids) dbg.coarse_ids[qi * c.n_coarse + i] = qkey_id(wkk);
+        if (dbg.coarse_dq) dbg.coarse_dq[qi * c.n_coarse + i] = (int32_t)qkey_d(wkk);
+      }
+    }
+    if (has_dbg) {
+      for (int i = nc + lane; i < c.n_coarse; i += 32) {
+        if (dbg.coarse_ids) dbg.coarse_ids[qi * c.n_coarse + i] = -1;
+        if (dbg.coarse_dq) dbg.coarse_dq[qi * c.n_coarse + i] = -1;
+      }
+    }
+    __syncwarp();
+    // 4-7. Stage 2, early termination, Stage 3, assembly
+    finish_query(ix, c, qf, cid, nc, akeys, rkeys, qi, out_ids, out_dist, dbg, has_dbg != 0, lane, cnt);
+    if (has_dbg && lane == 0) {
+      if (dbg.counters)
+        for (int t = 0; t < AQR_NCOUNT; ++t) dbg.counters[qi * AQR_NCOUNT + t] = cnt[t];
+      if (dbg.totals)
+        for (int t = 0; t < AQR_NCOUNT; ++t) atomicAdd(reinterpret_cast<unsigned long long*>(dbg.totals + t),
+                                                       (unsigned long long)cnt[t]);
+    }
+    __syncwarp();
+  }
+}
+
+// Stages 2 / ET / 3 / assembly alone, one warp per query
+__global__ void __launch_bounds__(128) rerank_kernel(IndexView ix, SearchCfg c, const float* __restrict__ q,
+                                                     int64_t nq, int64_t ld_q, const int32_t* __restrict__ cand,
+                                                     int32_t n_cand, int32_t* __restrict__ out_ids,
+                                                     float* __restrict__ out_dist, int per_warp, int o_reg) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (qi >= nq) return;
+  uint8_t* wb = smem + (threadIdx.x >> 5) * per_warp;
+  float* qf = reinterpret_cast<float*>(wb);
+  int32_t* cid = reinterpret_cast<int32_t*>(wb + o_reg);
+  load_query(ix, q, ld_q, qi, qf, nullptr, lane);
+  // the list ends at the first -1
+  int nc = n_cand;
+  for (int b = 0; b < n_cand; b += 32) {
+    const int i = b + lane;
+    const bool end = i < n_cand && __ldg(cand + qi * n_cand + i) < 0;
+    const uint32_t mk = __ballot_sync(kFull, end);
+    if (mk) { nc = b + __ffs(mk) - 1; break; }
+  }
+  for (int i = lane; i < nc; i += 32) cid[i] = __ldg(cand + qi * n_cand + i);
+  __syncwarp();
+  uint64_t* akeys = reinterpret_cast<uint64_t*>(wb + o_reg + al16(4 * n_cand));
+  uint64_t* rkeys = akeys + n_cand;
+  aqr_debug none{};
+  SearchCfg cc = c;
+  cc.n_coarse = n_cand;
+  finish_query(ix, cc, qf, cid, nc, akeys, rkeys, qi, out_ids, out_dist, none, false, lane, nullptr);
+}
+
+template <int LPR, int CPL>
+cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
+                     int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
+                     cudaStream_t s) {
+  const Layout L = make_layout(ix, c);
+  const size_t smem = (size_t)L.per_warp * wpb;
+  auto kern = search_kernel<LPR, CPL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int64_t want = (nq + wpb - 1) / wpb;
+  int64_t grid = (int64_t)nsm * per_sm;
+  if (want < grid) grid = want;
+  if (grid < 1) grid = 1;
+  aqr_debug d{};
+  if (dbg) d = *dbg;
+  kern<<<(unsigned)grid, wpb * 32, smem, s>>>(ix, c, L, q, nq, ld_q, out_ids, out_dist, d, dbg ? 1 : 0, counter);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int wpb) {
+  return (size_t)make_layout(ix, c).per_warp * wpb;
+}
+
+cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
+                          int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
+                          cudaStream_t s) {
+  const int nch = ix.d_pad >> 4;
+  int lpr = 1;
+  while (lpr < nch && lpr < 32) lpr <<= 1;
+  const int cpl = (nch + lpr - 1) / lpr;
+  switch (lpr) {
+    case 1: return launch_t<1, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
+    case 2: return launch_t<2, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
+    case 4: return launch_t<4, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
+    case 8: return launch_t<8, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
+    case 16: return launch_t<16, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
+    default:
+      if (cpl == 1) return launch_t<32, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
+      if (cpl == 2) return launch_t<32, 2>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
+      if (cpl <= 4) return launch_t<32, 4>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
+      return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_rerank(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
+                          const int32_t* cand, int32_t n_cand, int32_t* out_ids, float* out_dist,
+                          cudaStream_t s) {
+  const int wpb = 4;
+  const int o_reg = al16(4 * ix.d4);
+  const int per_warp = o_reg + al16(4 * n_cand) + al16(16 * n_cand + 16);
+  const size_t smem = (size_t)per_warp * wpb;
+  cudaError_t e = cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = (nq + wpb - 1) / wpb;
+  rerank_kernel<<<(unsigned)grid, wpb * 32, smem, s>>>(ix, c, q, nq, ld_q, cand, n_cand, out_ids, out_dist,
+                                                       per_warp, o_reg);
+  return cudaGetLastError();
+}
+
+}  // namespace aqr

@@ -1,0 +1,73 @@
+"""Test cases: seeded inputs (synth) -> oracle quantizer + codes -> host-built HNSW graph.
+
+The graph is built by the host builder from the ORACLE's codes, so no oracle input comes
+from the CUDA path.  Cached per process."""
+from __future__ import annotations
+
+import dataclasses
+import functools
+
+import numpy as np
+
+import oracle
+import synth
+from paper_2602_21600_b200 import graph as G
+
+
+@dataclasses.dataclass
+class Case:
+    name: str
+    w: synth.Workload
+    sample: np.ndarray
+    quant: oracle.Quant
+    codes: np.ndarray
+    graph: G.Graph
+    ix: oracle.Index
+    delta_override: float | None
+
+
+def _mk(name, w, delta_override=None, M=None, efc=None, p_max=5.0):
+    sample = synth.density_sample(len(w.x), seed=w.seed, cfg=w.name if w.name in synth.CFG_IDS else "tiny")
+    quant = oracle.train(w.x, sample, p_max=p_max,
+                         delta_override=float("nan") if delta_override is None else delta_override)
+    codes = oracle.encode(w.x, quant)
+    if M is None:
+        M, efc = G.adapt_params(w.M0, w.efc0, quant.delta, 0.0)
+    g = G.build_hnsw(codes, M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg="tiny"), n_threads=4)
+    return Case(name, w, sample, quant, codes, g, oracle.Index(w.x, codes, quant, g, w.metric), delta_override)
+
+
+@functools.lru_cache(maxsize=None)
+def case(name: str) -> Case:
+    if name == "tiny7":
+        return _mk(name, synth.gen_tiny(n=600, d=7, nq=24), M=6, efc=40)
+    if name == "tiny100ip":
+        return _mk(name, synth.gen_tiny(n=900, d=100, nq=24, metric="ip"), M=8, efc=48)
+    if name == "tiny960":
+        return _mk(name, synth.gen_tiny(n=300, d=960, nq=8), M=8, efc=40)
+    if name == "tiny33":
+        return _mk(name, synth.gen_tiny(n=700, d=33, nq=24), M=10, efc=50)
+    if name == "grid":
+        return _mk(name, synth.gen_grid(n=800, d=16, nq=24), delta_override=0.0, M=8, efc=64)
+    if name == "c1":
+        w = synth.gen_c1()
+        return _mk(name, w, M=None)
+    if name == "c1small":
+        w = synth.gen_c1(n=3000, nq=40)
+        return _mk(name, w, M=12, efc=64)
+    if name == "c2slice":
+        w = synth.gen_c2(n=60_000, nq=64)
+        return _mk(name, w, M=20, efc=100)
+    raise KeyError(name)
+
+
+def near(a, b, rel=1e-5, metric="l2"):
+    """fp32 agreement within `rel` relative (north_star: 1e-5).  For the inner-product metric the
+    distance is 1 - <q,x> (R12); its rounding error is that of the dot product, so the
+    tolerance is relative to max(|d|, |<q,x>|) (R19)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    scale = np.maximum(np.abs(a), np.abs(b))
+    if metric == "ip":
+        scale = np.maximum(scale, np.maximum(np.abs(1.0 - a), np.abs(1.0 - b)))
+    return np.abs(a - b) <= rel * scale + 1e-30
