@@ -1,0 +1,523 @@
+"""bench.py -- QPS at recall@10 >= 0.98 of the B200-native AQR-HNSW search (BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C2] [--ef auto|E] [--impl aqr|reference]
+  (N > 1: launched with torch.distributed.run, one process per GPU, NCCL)
+
+A "step" is one pass of the whole hot path (aqr_search: query quantization, greedy descent,
+layer-0 beam, Stage 2, early termination, Stage 3, assembly) over this rank's slice of the
+query batch.  C1-C4 replicate the index on every GPU and split the queries (weak scaling:
+each rank searches the full 10k query set, so per-GPU work is fixed as N grows; no data-path
+collective).  Index construction (generation, GPU encode, host HNSW build, upload) happens
+before the timed region.
+
+The JSON line carries `roofline` (the search kernel against the measured HBM copy bandwidth,
+algorithmic bytes per DESIGN.md "Bytes per query"), `cpu_baseline` (the CPU oracle on a
+bounded query sample, rank 0, N = 1), `e2e` (through the public API with host buffers and
+the H2D/D2H copies inside the timed region) and `clocks` (nvidia-smi during the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+EF_GRID = [16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 768, 1024]
+# per-config quantizer window P_max (never given by the paper; R4) and the
+# fixed HNSW construction inputs of BASELINE.json
+P_MAX = {"C1": 5.0, "C2": 0.2, "C3": 5.0, "C4": 5.0, "C5": 5.0}
+TARGET_RECALL = 0.98
+LAYOUT = "auto"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------------------------
+# distributed plumbing
+# --------------------------------------------------------------------------------------------
+def dist_init(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(np.asarray(v, dtype=np.float64), device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.cpu().numpy()
+
+
+def bcast_np(a, world, rank, dtype):
+    """Broadcast a host array from rank 0 (shape broadcast first)."""
+    if world == 1:
+        return a
+    import torch
+    import torch.distributed as dist
+    shp = torch.zeros(4, dtype=torch.int64, device="cuda")
+    if rank == 0:
+        s = list(a.shape) + [0] * (4 - a.ndim)
+        shp[:] = torch.tensor(s)
+        shp[3] = a.ndim
+    dist.broadcast(shp, 0)
+    nd = int(shp[3].item())
+    shape = tuple(int(v) for v in shp[:nd].tolist())
+    t = torch.from_numpy(np.ascontiguousarray(a)).cuda() if rank == 0 else torch.empty(shape, dtype=dtype, device="cuda")
+    dist.broadcast(t, 0)
+    return t.cpu().numpy()
+
+
+# --------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# --------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.p = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._rd, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _rd(self):
+        for ln in self.p.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(2)
+        except Exception:
+            self.p.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------------
+# workload + index construction (outside the timed region)
+# --------------------------------------------------------------------------------------------
+def make_workload(cfg, scale, nq):
+    import synth
+    return synth.gen_config(cfg, scale=scale, nq=nq)
+
+
+def build_index(w, cfg, rank, world, threads):
+    import torch
+    import synth
+    import paper_2602_21600_b200 as aqr
+    from paper_2602_21600_b200 import graph as G
+    t0 = time.time()
+    x = torch.from_numpy(w.x).cuda()
+    sample_np = synth.density_sample(len(w.x), seed=w.seed, cfg=cfg)
+    sample = torch.from_numpy(sample_np).cuda()
+    codes, quant = aqr.encode(x, sample_idx=sample, p_max=P_MAX[cfg], want_rho=True)
+    torch.cuda.synchronize()
+    t_enc = time.time() - t0
+    rho = quant.rho.cpu().numpy()
+    wj = G.density_weights(w.x[sample_np], rho)
+    eta = G.eta_of(wj)
+    M, efc = G.adapt_params(w.M0, w.efc0, quant.delta, eta)
+    t1 = time.time()
+    if rank == 0:
+        g = G.build_hnsw(codes.cpu().numpy(), M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg=cfg), threads)
+        arrs = [g.levels, g.upper_off, g.adj0, g.adj_upper, np.array([g.entry_point, g.max_level], np.int64)]
+    else:
+        arrs = [None] * 5
+    if world > 1:
+        dts = [torch.int32, torch.int64, torch.int32, torch.int32, torch.int64]
+        arrs = [bcast_np(a, world, rank, dt) for a, dt in zip(arrs, dts)]
+        g = G.Graph(M, efc, arrs[0], arrs[1], arrs[2], arrs[3], int(arrs[4][0]), int(arrs[4][1]))
+    t_build = time.time() - t1
+    ix = aqr.upload_index(codes, x, quant, g, metric=w.metric, layout=LAYOUT)
+    info = dict(layout=ix.layout, delta=quant.delta, eta=eta, M=M, efc=efc, p_max=P_MAX[cfg], p_low=quant.p_low, p_high=quant.p_high,
+                encode_s=round(t_enc, 2), build_s=round(t_build, 2), max_level=g.max_level,
+                index_bytes=ix.device_bytes())
+    return x, codes, quant, g, ix, info
+
+
+def bytes_per_query(tot, nq, d, k):
+    """Algorithmic bytes from the kernel counters:
+    query 4d + adjacency 4(deg+1) per expansion (all layers) + d per distinct code evaluation
+    (all layers; re-evaluations after a visited-hash miss excluded) + N_c d (Stage 2 re-read)
+    + 4d per exact re-rank + 8k output."""
+    exp, deg, ev, uexp, udeg, uev, nc, depth, et, na, fails = [float(v) for v in tot]
+    b = (4 * d * nq + 4 * (deg + exp) + 4 * (udeg + uexp) + d * (ev - fails + uev) + d * nc + 4 * d * depth
+         + 8 * k * nq)
+    return b / nq
+
+
+# --------------------------------------------------------------------------------------------
+# the AQR arm
+# --------------------------------------------------------------------------------------------
+def run_aqr(args):
+    import torch
+    import paper_2602_21600_b200 as aqr
+    from paper_2602_21600_b200 import evaluate as E
+
+    rank, world, local = dist_init(args.gpus)
+    cfg = args.config
+    w = make_workload(cfg, args.scale, args.nq)
+    k = w.k
+    nq = len(w.q)
+    lo, hi = rank * nq // world, (rank + 1) * nq // world
+    if args.weak:
+        lo, hi = 0, nq  # weak scaling: every rank searches the full query set
+    q_host = np.ascontiguousarray(w.q[lo:hi])
+    q = torch.from_numpy(q_host).cuda()
+    x, codes, quant, g, ix, info = build_index(w, cfg, rank, world, args.threads)
+    if rank == 0:
+        log(f"[bench] {cfg} n={len(w.x)} d={w.x.shape[1]} nq={nq} index: {info}")
+
+    # ground truth for this rank's queries, then the ef sweep (recall summed over ranks)
+    gt_ids, gt_d = E.ground_truth(x, q, k, w.metric)
+    sweep = []
+    chosen = None
+    grid = EF_GRID if args.ef == "auto" else [int(args.ef)]
+    for ef in grid:
+        m = aqr.ef_mapping(ef, k)
+        p = aqr.make_params(k, **m)
+        s = aqr.Searcher(ix, len(q), p)
+        s.run(q)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        s.run(q)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        ids = s.ids.clone()
+        ed = E.exact_dist(x, q, ids, w.metric).cpu().numpy()
+        ov, ta = E.recall(ids.cpu().numpy(), gt_ids, ed, gt_d, k)
+        tot = allreduce_sum([ov * len(q), ta * len(q), len(q)], world)
+        ov_all, ta_all = tot[0] / tot[2], tot[1] / tot[2]
+        ms_max = allreduce_max(ms, world)
+        sweep.append(dict(ef=ef, n_coarse=m["n_coarse"], n_rerank=m["n_rerank"], recall=round(ta_all, 4),
+                          recall_id=round(ov_all, 4), qps=round(float(tot[2]) / (ms_max / 1e3), 1)))
+        if rank == 0:
+            log(f"[bench] sweep {sweep[-1]}")
+        if ta_all >= TARGET_RECALL and chosen is None:
+            chosen = ef
+            if args.ef == "auto" and not args.full_sweep:
+                break
+    if chosen is None:
+        chosen = grid[-1]
+    m = aqr.ef_mapping(chosen, k)
+    vb_results = []
+    best_vb, best_ms = 0, float("inf")
+    for vb in args.vbits:
+        p = aqr.make_params(k, **m, visited_bits=vb)
+        s = aqr.Searcher(ix, len(q), p)
+        s.run(q)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(3):
+            s.run(q)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = allreduce_max(ev0.elapsed_time(ev1) / 3, world)
+        vb_results.append(dict(visited_bits=vb, ms=round(ms, 3)))
+        if ms < best_ms:
+            best_vb, best_ms = vb, ms
+    if rank == 0 and len(args.vbits) > 1:
+        log(f"[bench] visited_bits sweep {vb_results} -> {best_vb}")
+    p = aqr.make_params(k, **m, visited_bits=best_vb)
+    s = aqr.Searcher(ix, len(q), p)
+    # counters for the roofline (separate, untimed run with the stats path)
+    s.totals.zero_()
+    s.run(q, stats=True)
+    torch.cuda.synchronize()
+    tot_counters = s.totals.cpu().numpy()
+    bq = bytes_per_query(tot_counters, len(q), w.x.shape[1], k)
+
+    # ---- device-timed region: W warm-up steps, then K steps bracketed by barrier + sync ----
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        s.run(q)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = Clocks(local)
+    clocks.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for a, b in evs:
+        a.record(stream)
+        s.run(q)
+        b.record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    launch_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    total_ms = allreduce_max(total_ms, world)
+    ms_per_step = total_ms / args.steps
+    queries_per_step_all = len(q) * world
+    value = queries_per_step_all / (ms_per_step / 1e3)
+
+    # ---- end to end through the public API: pinned host queries in, host results out ----
+    qh = torch.from_numpy(q_host).pin_memory()
+    ids_h = torch.empty((len(q), k), dtype=torch.int32).pin_memory()
+    dist_h = torch.empty((len(q), k), dtype=torch.float32).pin_memory()
+    qd = torch.empty_like(q)
+    for _ in range(2):
+        qd.copy_(qh, non_blocking=True)
+        s.run(qd)
+        ids_h.copy_(s.ids, non_blocking=True)
+        dist_h.copy_(s.dist, non_blocking=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        qd.copy_(qh, non_blocking=True)
+        s.run(qd)
+        ids_h.copy_(s.ids, non_blocking=True)
+        dist_h.copy_(s.dist, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = allreduce_max(e0.elapsed_time(e1) / args.steps, world)
+    e2e_val = queries_per_step_all / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (search_kernel: one launch per step) ----
+    import json as _json
+    peaks = {}
+    try:
+        peaks = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    bytes_launch = bq * len(q)
+    achieved = bytes_launch / (launch_ms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            tj = _json.load(open(tf))
+            if tj.get("config") == cfg and tj.get("ef") == chosen and tj.get("nq") == len(q):
+                traffic = tj.get("bytes_per_launch")
+        except Exception:
+            pass
+
+    # ---- CPU oracle baseline: rank 0, N = 1, bounded query sample ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(w, cfg, quant, codes, g, m, k, args.cpu_seconds, s)
+
+    if rank == 0:
+        line = {
+            "metric": "QPS at recall@10>=0.98", "value": round(value, 1), "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8+int32+f32",
+            "data": "synthetic (seeded, BASELINE.json config recipe; paper datasets unavailable)",
+            "config": {"workload": f"{cfg}: {len(w.x)} x {w.x.shape[1]} {w.metric}, {nq} queries, k={k}",
+                       "ef": chosen, "n_coarse": m["n_coarse"], "n_rerank": m["n_rerank"],
+                       "recall@10": next(z["recall"] for z in sweep if z["ef"] == chosen) if any(
+                           z["ef"] == chosen for z in sweep) else None,
+                       "visited_bits": best_vb, "visited_bits_sweep": vb_results, "queries_per_rank": len(q), "parallelism": f"replicated index, dp{world}",
+                       "l2": "index (codes+adjacency+fp32) > 126 MB L2; no flush", **info},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "bytes_per_query": round(bq, 1), "peak_source": peak_src,
+                         "kernel": "search_kernel", "kernel_ms": round(launch_ms, 4)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_val, 1), "unit": "queries/s",
+                    "h2d_bytes_per_step": int(q_host.nbytes),
+                    "d2h_bytes_per_step": int(ids_h.numel() * 4 + dist_h.numel() * 4)},
+            "gpu_launches": args.steps,
+            "clocks": clk,
+            "ef_sweep": sweep,
+            "counters_per_query": {n: round(float(v) / len(q), 2) for n, v in zip(aqr.COUNTER_NAMES, tot_counters)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_baseline(w, cfg, quant, codes, g, m, k, seconds, searcher):
+    """The CPU oracle as it stands, single thread, on a bounded sample of the same queries.
+    The oracle trains its own quantizer and encodes the base itself; the codes are compared
+    byte for byte with the GPU's (full-size parity) before the oracle searches the same graph."""
+    import oracle
+    import synth
+    t0 = time.time()
+    sample = synth.density_sample(len(w.x), seed=w.seed, cfg=cfg)
+    o_quant = oracle.train(w.x, sample, p_max=P_MAX[cfg])
+    o_codes = oracle.encode(w.x, o_quant)
+    codes_equal = bool(np.array_equal(o_codes, codes.cpu().numpy()))
+    t_train = time.time() - t0
+    oix = oracle.Index(w.x, o_codes, o_quant, g, w.metric)
+    n_try = 8
+    t0 = time.time()
+    oracle.search(oix, w.q[:n_try], k, **m)
+    per_q = (time.time() - t0) / n_try
+    n_s = int(max(n_try, min(len(w.q), seconds / max(per_q, 1e-6))))
+    t0 = time.time()
+    o_ids, _ = oracle.search(oix, w.q[:n_s], k, **m)
+    el = time.time() - t0
+    g_ids = searcher.ids[:n_s].cpu().numpy()
+    return {"value": round(n_s / el, 2), "unit": "queries/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {n_s} of {len(w.q)} queries, same graph/ef ({el:.1f} s single-threaded C oracle)",
+            "codes_equal_full_size": codes_equal, "oracle_train_s": round(t_train, 1),
+            "ids_equal_frac": round(float((o_ids == g_ids).all(1).mean()), 4)}
+
+
+# --------------------------------------------------------------------------------------------
+# the reference arm: the CPU oracle as it stands (this tier has no reference implementation)
+# --------------------------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    from paper_2602_21600_b200 import graph as G
+    cfg = args.config
+    w = make_workload(cfg, args.scale, args.nq)
+    k = w.k
+    sample = synth.density_sample(len(w.x), seed=w.seed, cfg=cfg)
+    t0 = time.time()
+    rho = oracle.density(w.x, sample)
+    delta = oracle.delta(rho)
+    quant = oracle.train(w.x, sample, p_max=P_MAX[cfg], delta_override=delta)
+    codes = oracle.encode(w.x, quant)
+    eta = G.eta_of(G.density_weights(w.x[sample], rho))
+    M, efc = G.adapt_params(w.M0, w.efc0, quant.delta, eta)
+    g = G.build_hnsw(codes, M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg=cfg), args.threads)
+    log(f"[reference] index built in {time.time() - t0:.1f} s")
+    ef = 256 if args.ef == "auto" else int(args.ef)
+    m = G_ef_mapping(ef, k)
+    oix = oracle.Index(w.x, codes, quant, g, w.metric)
+    t0 = time.time()
+    oracle.search(oix, w.q[:4], k, **m)
+    per_q = max((time.time() - t0) / 4, 1e-6)
+    per_step = int(max(1, min(len(w.q), args.cpu_seconds / max(1, args.steps + args.warmup) / per_q)))
+    pos = 0
+    for _ in range(args.warmup):
+        oracle.search(oix, w.q[pos:pos + per_step], k, **m)
+    t0 = time.time()
+    for _ in range(args.steps):
+        oracle.search(oix, w.q[:per_step], k, **m)
+    el = time.time() - t0
+    v = per_step * args.steps / el
+    line = {"impl": "reference", "metric": "QPS at recall@10>=0.98", "value": round(v, 2), "unit": "queries/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(el / args.steps * 1e3, 2), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8+int32+f32", "data": "synthetic",
+            "config": {"workload": f"{cfg}: {len(w.x)} x {w.x.shape[1]} {w.metric}, {len(w.q)} queries, k={k}",
+                       "ef": ef, **m},
+            "cpu_baseline": {"value": round(v, 2), "unit": "queries/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{per_step} queries per step, single-threaded C oracle"},
+            "e2e": {"value": round(v, 2), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def G_ef_mapping(ef, k):
+    import oracle
+    return oracle.ef_mapping(ef, k)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="aqr", choices=["aqr", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--scale", type=float, default=1.0, help="fraction of the config's base size")
+    ap.add_argument("--nq", type=int, default=None)
+    ap.add_argument("--ef", default="auto")
+    ap.add_argument("--full-sweep", action="store_true")
+    ap.add_argument("--vbits", type=lambda v: [int(t) for t in v.split(",")], default=[0],
+                    help="visited-hash sizes (log2 slots, 0 = auto) tried at the chosen ef; fastest is timed")
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--split", dest="weak", action="store_false",
+                    help="split one query batch across ranks instead of every rank searching all queries")
+    ap.add_argument("--layout", default="auto", choices=["auto", "gather", "inline"])
+    args = ap.parse_args()
+    global LAYOUT
+    LAYOUT = args.layout
+    if args.warmup < 3:
+        log("[bench] warm-up raised to 3 (timing rule)")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_aqr(args)
+
+
+if __name__ == "__main__":
+    main()

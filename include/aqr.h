@@ -108,7 +108,19 @@ typedef struct {
                                 layer L (1 <= L <= level) of node v is row upper_off[v] + L - 1 */
   const int32_t *adj_upper;  /* host [upper_rows x M], -1 padded (may be NULL if upper_rows == 0) */
   int64_t upper_rows;
+  int32_t layout;            /* AQR_LAYOUT_AUTO / _GATHER / _INLINE (see below) */
 } aqr_index_desc;
+
+/* Layer-0 layout of the uploaded index.
+ *  GATHER: adjacency rows [n x 2M] int32 and the code array [n x d_pad]; an expansion reads
+ *          the row, then gathers one code row per neighbour (two dependent DRAM round trips).
+ *  INLINE: one contiguous block per node = its layer-0 neighbour ids followed by the codes of
+ *          those neighbours (n x 2M x d_pad bytes, ~7 GB for 1M x 128 at M = 27); an expansion
+ *          is ONE bulk (TMA) copy of that block into shared memory, prefetched while the
+ *          previous expansion's merge runs.  Uses HBM capacity to remove a round trip.
+ *  AUTO:   INLINE when the blocks fit in 40% of the free device memory, else GATHER.
+ * Both layouts give identical results (same visit order, same ids). */
+enum { AQR_LAYOUT_AUTO = 0, AQR_LAYOUT_GATHER = 1, AQR_LAYOUT_INLINE = 2 };
 
 /* Copy the index into library-owned device buffers re-laid-out for the search kernel
  * (code rows of d_pad bytes, fp32 rows padded to a multiple of 4 floats, layer-0 rows padded
@@ -119,6 +131,8 @@ aqr_status aqr_upload_index(const aqr_index_desc *desc, aqr_index **out, aqr_str
 void aqr_index_free(aqr_index *ix);
 /* bytes of device memory owned by the index */
 size_t aqr_index_device_bytes(const aqr_index *ix);
+/* the layout chosen at upload (AQR_LAYOUT_GATHER or AQR_LAYOUT_INLINE) */
+int32_t aqr_index_layout(const aqr_index *ix);
 
 /* ------------------------------------------------------------------------------------ */
 /* aqr_search -- Alg2 fused: quantize query, Stage 1 (greedy upper layers + layer-0 beam on */

@@ -43,7 +43,7 @@ class IndexDesc(C.Structure):
                 ("codes", C.c_void_p), ("d_pad", C.c_int32), ("base", C.c_void_p), ("ld_base", C.c_int64),
                 ("min_j", C.c_void_p), ("scale_j", C.c_void_p), ("M", C.c_int32), ("max_level", C.c_int32),
                 ("entry_point", C.c_int32), ("adj0", C.c_void_p), ("upper_off", C.c_void_p),
-                ("adj_upper", C.c_void_p), ("upper_rows", C.c_int64)]
+                ("adj_upper", C.c_void_p), ("upper_rows", C.c_int64), ("layout", C.c_int32)]
 
 
 class SearchParams(C.Structure):
@@ -58,7 +58,9 @@ class Debug(C.Structure):
                 ("exact_d", C.c_void_p), ("counters", C.c_void_p), ("totals", C.c_void_p)]
 
 
-EXPORTS = ["aqr_encode", "aqr_upload_index", "aqr_index_free", "aqr_index_device_bytes", "aqr_search_workspace_size",
+LAYOUTS = {"auto": 0, "gather": 1, "inline": 2}
+EXPORTS = ["aqr_encode", "aqr_upload_index", "aqr_index_free", "aqr_index_device_bytes", "aqr_index_layout",
+           "aqr_search_workspace_size",
            "aqr_search", "aqr_rerank", "aqr_merge_topk", "aqr_last_error", "aqr_version"]
 
 _lib = None
@@ -80,6 +82,7 @@ def lib():
         L.aqr_version.restype = C.c_char_p
         L.aqr_index_device_bytes.restype = C.c_size_t
         L.aqr_search_workspace_size.restype = C.c_size_t
+        L.aqr_index_layout.restype = C.c_int32
         for f in ["aqr_encode", "aqr_upload_index", "aqr_search", "aqr_rerank", "aqr_merge_topk"]:
             getattr(L, f).restype = C.c_int
         _lib = L
@@ -188,6 +191,10 @@ class Index:
             raise AqrError("index already freed")
         return self._h
 
+    @property
+    def layout(self) -> str:
+        return {1: "gather", 2: "inline"}.get(int(lib().aqr_index_layout(self.handle)), "?")
+
     def device_bytes(self) -> int:
         return int(lib().aqr_index_device_bytes(self.handle))
 
@@ -203,7 +210,7 @@ class Index:
             pass
 
 
-def upload_index(codes, base, quant: Quantizer, graph, metric="l2", id_base=0, stream=None) -> Index:
+def upload_index(codes, base, quant: Quantizer, graph, metric="l2", id_base=0, layout="auto", stream=None) -> Index:
     """aqr_upload_index: codes [n, d_pad] u8 CUDA, base [n, d] fp32 CUDA, graph (host arrays)."""
     torch = _torch()
     _dev(codes, torch.uint8, "codes")
@@ -222,6 +229,7 @@ def upload_index(codes, base, quant: Quantizer, graph, metric="l2", id_base=0, s
     D.upper_off = upper_off.ctypes.data
     D.adj_upper = adj_upper.ctypes.data if adj_upper.size else None
     D.upper_rows = adj_upper.shape[0] if adj_upper.size else 0
+    D.layout = LAYOUTS[layout]
     h = C.c_void_p()
     st = lib().aqr_upload_index(C.byref(D), C.byref(h), _stream(stream))
     _check(st, "aqr_upload_index")

@@ -9,6 +9,7 @@
 
 struct aqr_index {
   aqr::IndexView v;
+  int32_t layout = AQR_LAYOUT_GATHER;
   std::vector<void*> allocs;
   size_t bytes = 0;
 };
@@ -127,6 +128,7 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   AQR_CHECK_ARG(D.entry_point >= 0 && D.entry_point < D.n, "upload: entry_point out of range");
   AQR_CHECK_ARG(D.upper_rows >= 0 && (D.upper_rows == 0 || D.adj_upper), "upload: adj_upper missing");
   AQR_CHECK_ARG(D.id_base >= 0 && D.id_base + D.n <= (int64_t(1) << 31), "upload: id_base + n must fit int32");
+  AQR_CHECK_ARG(D.layout >= AQR_LAYOUT_AUTO && D.layout <= AQR_LAYOUT_INLINE, "upload: bad layout");
   const int64_t n = D.n;
   const int32_t cap0 = 2 * D.M, M = D.M;
   // host-side validation of the graph
@@ -207,6 +209,32 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   V.adj0 = a0;
   V.adj_up = au;
   V.up_off = uo;
+  V.blk = nullptr;
+  V.blk_ids = round_up(4 * cap0, 16);
+  V.blk_bytes = V.blk_ids + cap0 * D.d_pad;
+  V.blk_stride = (V.blk_bytes + 127) / 128 * 128;
+  // layer-0 layout (include/aqr.h): INLINE blocks when they fit
+  const size_t blk_total = (size_t)n * (size_t)V.blk_stride;
+  bool inl = D.layout == AQR_LAYOUT_INLINE;
+  if (D.layout == AQR_LAYOUT_AUTO) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) inl = blk_total <= (size_t)(0.4 * (double)free_b);
+  }
+  if (inl) {
+    uint8_t* blk = (uint8_t*)alloc(blk_total);
+    if (!blk) {
+      set_error("aqr: upload: device allocation of the INLINE layout failed (use AQR_LAYOUT_GATHER)");
+      return fail(AQR_E_OOM);
+    }
+    e = aqr::launch_build_inline(V, blk, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      aqr_status st = cuda_fail(e, "upload: inline layout");
+      return fail(st);
+    }
+    V.blk = blk;
+    ix->layout = AQR_LAYOUT_INLINE;
+  }
   *out = ix;
   return AQR_OK;
 }
@@ -218,6 +246,7 @@ void aqr_index_free(aqr_index* ix) {
 }
 
 size_t aqr_index_device_bytes(const aqr_index* ix) { return ix ? ix->bytes : 0; }
+int32_t aqr_index_layout(const aqr_index* ix) { return ix ? ix->layout : 0; }
 
 size_t aqr_search_workspace_size(const aqr_index*, int64_t, const aqr_search_params*) { return 256; }
 

@@ -23,6 +23,11 @@ struct IndexView {
   const int32_t* adj_up;  // [upper_rows x M]
   const int32_t* up_off;  // [n] (-1 for level-0 nodes)
   int32_t max_level, entry;
+  // INLINE layout (nullptr for GATHER): per node a block of blk_stride bytes =
+  // [cap0 int32 ids, padded to blk_ids bytes][cap0 code rows of d_pad bytes]
+  const uint8_t* blk;
+  int64_t blk_stride;
+  int32_t blk_ids, blk_bytes;  // blk_bytes = blk_ids + cap0 * d_pad (bulk-copy size)
 };
 
 struct SearchCfg {
@@ -53,5 +58,6 @@ cudaError_t launch_rerank(const IndexView& ix, const SearchCfg& c, const float* 
 cudaError_t launch_merge(const float* dist, const int32_t* ids, int32_t n_lists, int64_t nq, int32_t k,
                          float* out_dist, int32_t* out_ids, cudaStream_t s);
 size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int warps_per_block);
+cudaError_t launch_build_inline(const IndexView& ix, uint8_t* blk, cudaStream_t s);
 
 }  // namespace aqr

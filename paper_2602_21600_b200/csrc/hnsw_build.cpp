@@ -171,10 +171,11 @@ int64_t aqr_hnsw_levels(const double* u, int64_t n, int32_t M, int32_t* levels, 
 }
 
 // Build the graph.  adj0: [n x 2M] and adj_upper: [rows x M] are caller-allocated and are
-// filled with -1 padding.  out2 = {entry_point, max_level}.  Returns 0 on success.
+// filled with -1 padding.  out2 = {entry_point, max_level}.  batch_div: a batch holds at most
+// pos / batch_div nodes (0 = 32; a huge value gives sequential insertion).  Returns 0 on success.
 int aqr_hnsw_build(const uint8_t* codes, int64_t n, int32_t d_pad, const int32_t* levels,
                    const int64_t* upper_off, int32_t M, int32_t efc, int32_t n_threads,
-                   int32_t* adj0, int32_t* adj_upper, int64_t upper_rows, int32_t* out2) {
+                   int32_t* adj0, int32_t* adj_upper, int64_t upper_rows, int32_t* out2, int32_t batch_div) {
   if (!codes || n < 1 || M < 2 || efc < 1 || !adj0 || !out2) return 1;
   Graph g;
   g.n = n; g.d_pad = d_pad; g.M = M; g.cap0 = 2 * M; g.efc = efc; g.codes = codes;
@@ -194,9 +195,10 @@ int aqr_hnsw_build(const uint8_t* codes, int64_t n, int32_t d_pad, const int32_t
   g.max_level = levels[0];
   int64_t pos = 1;
   const int64_t kBatchCap = 4096;
+  if (batch_div <= 0) batch_div = 32;
   std::vector<std::vector<std::pair<int32_t, std::vector<int32_t>>>> sel;  // per batch item: (L, nbrs)
   while (pos < n) {
-    int64_t B = std::min<int64_t>(std::max<int64_t>(1, pos / 32), kBatchCap);
+    int64_t B = std::min<int64_t>(std::max<int64_t>(1, pos / batch_div), kBatchCap);
     B = std::min<int64_t>(B, n - pos);
     for (int64_t i = 0; i < B; ++i)
       if (levels[pos + i] > g.max_level) { B = (i == 0) ? 1 : i; break; }

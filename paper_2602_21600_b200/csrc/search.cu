@@ -78,6 +78,33 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
   return r;
 }
 
+// ---- mbarrier + bulk (TMA) copy helpers (sm_90+ PTX; UBLKCP in SASS) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// arrive (count 1) and announce `bytes` of transaction, then copy `bytes` global -> shared
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // number of keys in sorted a[0:n) strictly less than key
 __device__ __forceinline__ int lower_bound_u64(const uint64_t* a, int n, uint64_t key) {
   int lo = 0, hi = n;
@@ -103,8 +130,9 @@ __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t 
 // per-warp shared-memory layout
 // ------------------------------------------------------------------------------------
 struct Layout {
-  int o_qc, o_qf, o_w, o_h, o_nb, o_nd, o_cand, o_cs, per_warp;
-  int region;  // bytes of the hash region (reused by Stage 2/3)
+  int o_qc, o_qf, o_w, o_h, o_nb, o_nd, o_cand, o_cs, o_bar, per_warp;
+  int region;     // bytes of the hash / block-buffer region (reused by Stage 2/3)
+  int buf_bytes;  // INLINE: one staged block (128-byte aligned)
 };
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
@@ -115,15 +143,18 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c) {
   L.o_qc = o; o += al16(ix.d_pad);
   L.o_qf = o; o += al16(4 * ix.d4);
   L.o_w = o; o += al16(8 * (c.ef + 1));
-  int hb = 4 << c.hbits;
+  L.buf_bytes = (ix.blk_bytes + 127) & ~127;
+  int hb = ix.blk ? 2 * L.buf_bytes : (4 << c.hbits);
   int s23 = 20 * c.n_coarse + 32;
   L.region = hb > s23 ? hb : s23;
+  o = (o + 127) & ~127;
   L.o_h = o; o += al16(L.region);
   L.o_nb = o; o += al16(4 * ix.ld0);
   L.o_nd = o; o += al16(4 * ix.ld0);
   L.o_cand = o; o += al16(8 * ix.ld0);
   L.o_cs = o; o += al16(8 * ix.ld0);
-  L.per_warp = o;
+  L.o_bar = o; o += 16;
+  L.per_warp = (o + 127) & ~127;
   return L;
 }
 
@@ -173,8 +204,10 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const uint4 (&qr
 
 // ------------------------------------------------------------------------------------
 // visited set: open-addressing hash of node ids in shared memory.  A full probe window
-// reports "not visited" without inserting: a false negative only causes a re-evaluation,
-// which the W dedupe absorbs (R15).  False positives cannot occur.
+// reports "not visited" and overwrites the window's last slot (so the table keeps the most
+// recently seen ids): a false negative only causes a re-evaluation, which the W dedupe
+// absorbs (R15).  False positives cannot occur: a slot only ever holds
+// an id that was inserted, and a hit requires the exact id.
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ bool visit_new(uint32_t* h, int hbits, int32_t u, int& fails) {
   const uint32_t hmask = (1u << hbits) - 1u;
@@ -184,8 +217,10 @@ __device__ __forceinline__ bool visit_new(uint32_t* h, int hbits, int32_t u, int
     uint32_t old = atomicCAS(h + s, kEmpty, (uint32_t)u);
     if (old == kEmpty) return true;
     if (old == (uint32_t)u) return false;
-    s = (s + 1) & hmask;
+    if (p + 1 < kProbes) s = (s + 1) & hmask;
   }
+  // probe window full: overwrite its last slot (the table keeps the most recent ids)
+  atomicExch(h + s, (uint32_t)u);
   ++fails;
   return true;
 }
@@ -380,12 +415,58 @@ __device__ __forceinline__ void load_query(const IndexView& ix, const float* q, 
 // ------------------------------------------------------------------------------------
 // the fused search kernel
 // ------------------------------------------------------------------------------------
+// d^q for the rows of an INLINE block staged in shared memory (rows with id < 0 skipped)
 template <int LPR, int CPL>
+__device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, const uint4 (&qreg)[CPL], int qq,
+                                            const int32_t* ids, int m, int32_t* out, int lane) {
+  constexpr int G = 32 / LPR;
+  constexpr int U = CPL == 1 ? 4 : 2;
+  const int g = lane / LPR, sub = lane % LPR;
+  const int nch = d_pad >> 4;
+  for (int r0 = 0; r0 < m; r0 += G * U) {
+    uint4 buf[U][CPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = r0 + u * G + g;
+      const int id = r < m ? ids[r] : -1;
+      const uint4* row = reinterpret_cast<const uint4*>(codes_s + (r < m ? r : 0) * d_pad);
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) {
+        const int c = sub + LPR * t;
+        buf[u][t] = (id >= 0 && c < nch) ? row[c] : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      unsigned xx = 0, qx = 0;
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) {
+        const uint4 w = buf[u][t], qw = qreg[t];
+        xx = __dp4a(w.x, w.x, xx); qx = __dp4a(qw.x, w.x, qx);
+        xx = __dp4a(w.y, w.y, xx); qx = __dp4a(qw.y, w.y, qx);
+        xx = __dp4a(w.z, w.z, xx); qx = __dp4a(qw.z, w.z, qx);
+        xx = __dp4a(w.w, w.w, xx); qx = __dp4a(qw.w, w.w, qx);
+      }
+      int s = (int)xx - 2 * (int)qx;
+#pragma unroll
+      for (int off = LPR / 2; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+      const int r = r0 + u * G + g;
+      if (sub == 0 && r < m) out[r] = qq + s;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// the fused search kernel; INL selects the INLINE layer-0 layout (bulk-copied blocks,
+// next block prefetched during the merge) or the GATHER layout (row + per-code gathers,
+// shared-memory visited hash)
+// ------------------------------------------------------------------------------------
+template <int LPR, int CPL, bool INL>
 __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, Layout L, const float* __restrict__ q,
                                                      int64_t nq, int64_t ld_q, int32_t* __restrict__ out_ids,
                                                      float* __restrict__ out_dist, aqr_debug dbg, int has_dbg,
                                                      int* __restrict__ counter) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   uint8_t* wb = smem + (threadIdx.x >> 5) * L.per_warp;
   uint8_t* qc = wb + L.o_qc;
@@ -396,9 +477,20 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
   int32_t* nd = reinterpret_cast<int32_t*>(wb + L.o_nd);
   uint64_t* cand = reinterpret_cast<uint64_t*>(wb + L.o_cand);
   uint64_t* cs = reinterpret_cast<uint64_t*>(wb + L.o_cs);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wb + L.o_bar);
+  uint8_t* bufs[2] = {wb + L.o_h, wb + L.o_h + L.buf_bytes};
   const int sub = lane % LPR;
   const int nch = ix.d_pad >> 4;
   const int ef = c.ef;
+  uint32_t phase[2] = {0u, 0u};
+  if (INL) {
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+      fence_proxy_async();
+    }
+    __syncwarp();
+  }
 
   for (;;) {
     int64_t qi = 0;
@@ -455,26 +547,33 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
     }
 
     // 3. layer-0 beam (flag form)
-    {
+    int b = 0;
+    if (INL) {
+      if (lane == 0) {
+        fence_proxy_async();
+        bulk_load(bufs[0], ix.blk + (int64_t)cur * ix.blk_stride, (uint32_t)ix.blk_bytes, bar);
+        W[0] = qkey(dcur, cur);
+      }
+    } else {
       uint4* h4 = reinterpret_cast<uint4*>(hash);
       const int nh4 = (1 << c.hbits) >> 2;
       for (int t = lane; t < nh4; t += 32) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-    }
-    __syncwarp();
-    if (lane == 0) {
-      W[0] = qkey(dcur, cur);
-      visit_new(hash, c.hbits, cur, fails);
+      __syncwarp();
+      if (lane == 0) {
+        W[0] = qkey(dcur, cur);
+        visit_new(hash, c.hbits, cur, fails);
+      }
     }
     __syncwarp();
     int size = 1, cursor = 0, nexp = 0;
     for (;;) {
       // smallest unexpanded entry of W
       int pos = -1;
-      for (int b = cursor; b < size; b += 32) {
-        const int i = b + lane;
+      for (int bb = cursor; bb < size; bb += 32) {
+        const int i = bb + lane;
         const bool un = i < size && !(W[i] & 1ull);
         const uint32_t mk = __ballot_sync(kFull, un);
-        if (mk) { pos = b + __ffs(mk) - 1; break; }
+        if (mk) { pos = bb + __ffs(mk) - 1; break; }
       }
       if (pos < 0) break;
       const uint64_t wk = W[pos];
@@ -485,31 +584,77 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
         if (has_dbg && dbg.exp_ids && nexp < dbg.exp_cap) dbg.exp_ids[qi * dbg.exp_cap + nexp] = cnode;
       }
       ++nexp;
-      // neighbours not yet visited
-      int deg;
-      const int m = gather_row(ix.adj0 + (int64_t)cnode * ix.ld0, ix.cap0, nb, hash, c.hbits, fails, deg, lane);
-      cnt[1] += deg;
-      cnt[2] += m;
-      list_dists<LPR, CPL>(ix, qreg, qq, nb, m, nd, lane);
+      int m;
+      const int32_t* ids;
+      if (INL) {
+        // the block of cnode was bulk-copied into bufs[b] (prefetched)
+        mbar_wait(bar + b, phase[b]);
+        phase[b] ^= 1u;
+        ids = reinterpret_cast<const int32_t*>(bufs[b]);
+        m = ix.cap0;
+        int deg = 0;
+        for (int t0 = 0; t0 < m; t0 += 32) deg += __popc(__ballot_sync(kFull, t0 + lane < m && ids[t0 + lane] >= 0));
+        cnt[1] += deg;
+        cnt[2] += deg;
+        block_dists<LPR, CPL>(bufs[b] + ix.blk_ids, ix.d_pad, qreg, qq, ids, m, nd, lane);
+      } else {
+        // neighbours not yet visited
+        int deg;
+        m = gather_row(ix.adj0 + (int64_t)cnode * ix.ld0, ix.cap0, nb, hash, c.hbits, fails, deg, lane);
+        ids = nb;
+        cnt[1] += deg;
+        cnt[2] += m;
+        list_dists<LPR, CPL>(ix, qreg, qq, nb, m, nd, lane);
+      }
       __syncwarp();
-      // filter against max W (when full) and drop re-evaluations already in W
+      // filter against max W (when full) and drop re-evaluations already in W (R15)
       const uint64_t maxk = size >= ef ? (W[size - 1] & ~1ull) : ~0ull;
       int np = 0;
+      uint64_t cmin = ~0ull;
       for (int r0 = 0; r0 < m; r0 += 32) {
         const int r = r0 + lane;
         bool ok = false;
         uint64_t kk = 0;
         if (r < m) {
-          kk = qkey((uint32_t)nd[r], nb[r]);
-          ok = kk < maxk;
-          if (ok) {
-            const int lb = lower_bound_w(W, size, kk);
-            ok = !(lb < size && (W[lb] & ~1ull) == kk);
+          const int32_t id = ids[r];
+          if (id >= 0) {
+            kk = qkey((uint32_t)nd[r], id);
+            ok = kk < maxk;
+            if (ok) {
+              const int lb = lower_bound_w(W, size, kk);
+              ok = !(lb < size && (W[lb] & ~1ull) == kk);
+            }
           }
         }
         const uint32_t mk = __ballot_sync(kFull, ok);
-        if (ok) cand[np + __popc(mk & ((1u << lane) - 1u))] = kk;
+        if (ok) {
+          cand[np + __popc(mk & ((1u << lane) - 1u))] = kk;
+          cmin = kk < cmin ? kk : cmin;
+        }
         np += __popc(mk);
+      }
+      if (INL) {
+        // the next expansion is min(first unexpanded entry of W after pos, smallest candidate);
+        // start its bulk copy now so it overlaps the merge (prefetch only, never speculative)
+        cmin = warp_min_u64(cmin);
+        uint64_t kw = ~0ull;
+        for (int bb = pos + 1; bb < size; bb += 32) {
+          const int i = bb + lane;
+          const bool un = i < size && !(W[i] & 1ull);
+          const uint32_t mk = __ballot_sync(kFull, un);
+          if (mk) {
+            kw = W[bb + __ffs(mk) - 1];
+            break;
+          }
+        }
+        const uint64_t nxt = kw < cmin ? kw : cmin;
+        __syncwarp();
+        if (nxt != ~0ull && lane == 0) {
+          fence_proxy_async();
+          bulk_load(bufs[b ^ 1], ix.blk + (int64_t)qkey_id(nxt) * ix.blk_stride, (uint32_t)ix.blk_bytes,
+                    bar + (b ^ 1));
+        }
+        b ^= 1;
       }
       __syncwarp();
       if (np == 0) {
@@ -551,7 +696,7 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
 
     // debug: C with d^q
     const int nc = c.n_coarse < size ? c.n_coarse : size;
-    int32_t* cid = reinterpret_cast<int32_t*>(hash);
+    int32_t* cid = reinterpret_cast<int32_t*>(wb + L.o_h);
     uint64_t* akeys = reinterpret_cast<uint64_t*>(wb + L.o_h + al16(4 * nc));
     uint64_t* rkeys = akeys + nc;
     __syncwarp();
@@ -580,6 +725,24 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
                                                        (unsigned long long)cnt[t]);
     }
     __syncwarp();
+  }
+}
+
+// INLINE layout builder: one warp per node copies its ids and its neighbours' code rows
+__global__ void build_inline_kernel(IndexView ix, uint8_t* __restrict__ blk) {
+  const int lane = threadIdx.x & 31;
+  const int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (v >= ix.n) return;
+  uint8_t* out = blk + v * ix.blk_stride;
+  const int32_t* row = ix.adj0 + v * ix.ld0;
+  int32_t* oid = reinterpret_cast<int32_t*>(out);
+  for (int t = lane; t < ix.blk_ids / 4; t += 32) oid[t] = t < ix.cap0 ? row[t] : -1;
+  const int nch = ix.d_pad >> 4;
+  uint4* oc = reinterpret_cast<uint4*>(out + ix.blk_ids);
+  for (int e = lane; e < ix.cap0 * nch; e += 32) {
+    const int r = e / nch, ch = e - r * nch;
+    const int32_t u = row[r];
+    oc[e] = u >= 0 ? reinterpret_cast<const uint4*>(ix.codes + (int64_t)u * ix.d_pad)[ch] : make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -614,13 +777,13 @@ __global__ void __launch_bounds__(128) rerank_kernel(IndexView ix, SearchCfg c, 
   finish_query(ix, cc, qf, cid, nc, akeys, rkeys, qi, out_ids, out_dist, none, false, lane, nullptr);
 }
 
-template <int LPR, int CPL>
+template <int LPR, int CPL, bool INL>
 cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                      int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
                      cudaStream_t s) {
   const Layout L = make_layout(ix, c);
   const size_t smem = (size_t)L.per_warp * wpb;
-  auto kern = search_kernel<LPR, CPL>;
+  auto kern = search_kernel<LPR, CPL, INL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
@@ -652,18 +815,30 @@ cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* 
   int lpr = 1;
   while (lpr < nch && lpr < 32) lpr <<= 1;
   const int cpl = (nch + lpr - 1) / lpr;
+  const bool inl = ix.blk != nullptr;
+#define AQR_LAUNCH(L_, C_)                                                                               \
+  return inl ? launch_t<L_, C_, true>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)      \
+             : launch_t<L_, C_, false>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)
   switch (lpr) {
-    case 1: return launch_t<1, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
-    case 2: return launch_t<2, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
-    case 4: return launch_t<4, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
-    case 8: return launch_t<8, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
-    case 16: return launch_t<16, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
+    case 1: AQR_LAUNCH(1, 1);
+    case 2: AQR_LAUNCH(2, 1);
+    case 4: AQR_LAUNCH(4, 1);
+    case 8: AQR_LAUNCH(8, 1);
+    case 16: AQR_LAUNCH(16, 1);
     default:
-      if (cpl == 1) return launch_t<32, 1>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
-      if (cpl == 2) return launch_t<32, 2>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
-      if (cpl <= 4) return launch_t<32, 4>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s);
+      if (cpl == 1) AQR_LAUNCH(32, 1);
+      if (cpl == 2) AQR_LAUNCH(32, 2);
+      if (cpl <= 4) AQR_LAUNCH(32, 4);
       return cudaErrorInvalidValue;
   }
+#undef AQR_LAUNCH
+}
+
+cudaError_t launch_build_inline(const IndexView& ix, uint8_t* blk, cudaStream_t s) {
+  const int wpb = 8;
+  const int64_t grid = (ix.n + wpb - 1) / wpb;
+  build_inline_kernel<<<(unsigned)grid, wpb * 32, 0, s>>>(ix, blk);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_rerank(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,

@@ -38,8 +38,10 @@ def gpu_index():
             sample = torch.from_numpy(c.sample).cuda()
             codes, quant = aqr.encode(x, sample_idx=sample, p_max=5.0, delta_override=c.delta_override)
             torch.cuda.synchronize()
-            ix = aqr.upload_index(codes, x, quant, c.graph, metric=c.w.metric)
-            cache[name] = (c, codes, quant, ix)
+            ix = aqr.upload_index(codes, x, quant, c.graph, metric=c.w.metric, layout="gather")
+            ixi = aqr.upload_index(codes, x, quant, c.graph, metric=c.w.metric, layout="inline")
+            assert ix.layout == "gather" and ixi.layout == "inline"
+            cache[name] = (c, codes, quant, ix, ixi)
         return cache[name]
 
     return get
@@ -47,7 +49,7 @@ def gpu_index():
 
 @pytest.mark.parametrize("name", CASES)
 def test_encode_bit_exact(gpu_index, name):
-    c, codes, quant, _ = gpu_index(name)
+    c, codes, quant, _, _ = gpu_index(name)
     assert quant.delta == c.quant.delta
     np.testing.assert_array_equal(quant.min_j.cpu().numpy().view(np.uint32), c.quant.min_f.view(np.uint32))
     np.testing.assert_array_equal(quant.max_j.cpu().numpy().view(np.uint32), c.quant.max_f.view(np.uint32))
@@ -79,12 +81,14 @@ def _explained(o_ad, k, depth_or, p, o_fd, g_fd, metric):
     return bool(np.any(near(fd[1:], fd[:-1], 2e-5, metric)))
 
 
+@pytest.mark.parametrize("layout", ["gather", "inline"])
 @pytest.mark.parametrize("name", CASES)
 @pytest.mark.parametrize("ef", [16, 48, 96])
-def test_search_parity(gpu_index, name, ef):
+def test_search_parity(gpu_index, name, ef, layout):
     torch = _torch()
     aqr = _aqr()
-    c, codes, quant, ix = gpu_index(name)
+    c, codes, quant, ixg, ixi = gpu_index(name)
+    ix = ixg if layout == "gather" else ixi
     p = _params(c, ef)
     p.update(tau_gap=0.010, tau_ratio=1.008, early_term=True)
     q = c.w.q
@@ -126,7 +130,7 @@ def test_search_parity(gpu_index, name, ef):
 def test_rerank_split_equals_fused(gpu_index, name):
     torch = _torch()
     aqr = _aqr()
-    c, codes, quant, ix = gpu_index(name)
+    c, codes, quant, ix, _ = gpu_index(name)
     p = _params(c, 48)
     qd = torch.from_numpy(c.w.q).cuda()
     ids, d, tr = aqr.search(ix, qd, trace=True, **p)
@@ -162,7 +166,7 @@ def test_lossless_grid_equals_bruteforce(gpu_index):
     """lossless quantizer + exhaustive settings -> brute-force exact top-k."""
     torch = _torch()
     aqr = _aqr()
-    c, codes, quant, ix = gpu_index("grid")
+    c, codes, quant, ix, _ = gpu_index("grid")
     n = len(c.w.x)
     k = 5
     ids, d = aqr.search(ix, torch.from_numpy(c.w.q).cuda(), k=k, ef=n, n_coarse=n, n_rerank=n, early_term=False)

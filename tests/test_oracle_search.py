@@ -1,0 +1,333 @@
+"""Pins of the oracle's search path (Alg2) and of the host builder (-m "not gpu").
+
+Independent references: numpy brute force (exact and quantized), Malkov's heap-form
+SEARCH-LAYER (an independent implementation inside the oracle), hand-built
+graphs with hand-computed early-termination decisions, and invariants of the definitions.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from paper_2602_21600_b200 import graph as G
+from tests._cases import case
+
+
+def _bf_dq(codes, qcodes, n_c):
+    """numpy brute force: top-n_c by (d^q, id)."""
+    d = ((qcodes[:, None, :].astype(np.int64) - codes[None, :, :].astype(np.int64)) ** 2).sum(-1)
+    ids = np.arange(codes.shape[0])
+    out = []
+    for row in d:
+        o = np.lexsort((ids, row))[:n_c]
+        out.append(o)
+    return np.array(out), d
+
+
+def _bf_exact(x, q, k, metric="l2"):
+    if metric == "l2":
+        d = ((q[:, None, :].astype(np.float64) - x[None].astype(np.float64)) ** 2).sum(-1)
+    else:
+        d = 1.0 - q.astype(np.float64) @ x.T.astype(np.float64)
+    ids = np.arange(x.shape[0])
+    return np.array([np.lexsort((ids, r))[:k] for r in d]), d
+
+
+# ------------------------------------------------------------------------------------------
+# Stage 1 (O9-O10)
+# ------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["tiny7", "tiny33", "grid"])
+def test_exhaustive_beam_equals_bruteforce_dq(name):
+    """ef >= n on a connected graph: C = brute-force top-N_c by (d^q, id)."""
+    c = case(name)
+    n = len(c.w.x)
+    n_c = 20
+    ids, d, tr = oracle.search(c.ix, c.w.q, k=5, ef=n, n_coarse=n_c, n_rerank=n_c, early_term=False, trace=True)
+    qcodes = oracle.encode(c.w.q, c.quant)
+    ref, dq = _bf_dq(c.codes, qcodes, n_c)
+    np.testing.assert_array_equal(tr["coarse_ids"], ref)
+    np.testing.assert_array_equal(tr["coarse_dq"], np.take_along_axis(dq, ref, 1))
+
+
+@pytest.mark.parametrize("name", ["tiny7", "tiny33", "tiny100ip", "c1small"])
+@pytest.mark.parametrize("ef", [1, 8, 40])
+def test_heap_form_equals_flag_form(name, ef):
+    """Malkov's heap-form SEARCH-LAYER and the flag form expand the same sequence and end with
+    the same W."""
+    c = case(name)
+    k = min(ef, c.w.k)
+    kw = dict(k=k, ef=ef, n_coarse=ef, n_rerank=ef, early_term=False, trace=True)
+    a_ids, a_d, a = oracle.search(c.ix, c.w.q, beam_form=0, **kw)
+    b_ids, b_d, b = oracle.search(c.ix, c.w.q, beam_form=1, **kw)
+    np.testing.assert_array_equal(a["exp_ids"], b["exp_ids"])
+    np.testing.assert_array_equal(a["coarse_ids"], b["coarse_ids"])
+    np.testing.assert_array_equal(a_ids, b_ids)
+
+
+def test_self_query_returns_itself():
+    """A query equal to a stored vector is returned at rank 1 with distance 0."""
+    c = case("tiny33")
+    q = c.w.x[[3, 77, 310]]
+    ids, d = oracle.search(c.ix, q, k=1, ef=64, n_coarse=16, n_rerank=16)
+    np.testing.assert_array_equal(ids[:, 0], [3, 77, 310])
+    np.testing.assert_array_equal(d[:, 0], 0.0)
+
+
+def test_ef1_is_greedy_descent():
+    """ef = 1 degenerates to greedy descent: the result is a local minimum of d^q
+    over its layer-0 neighbourhood."""
+    c = case("tiny7")
+    ids, d, tr = oracle.search(c.ix, c.w.q, k=1, ef=1, n_coarse=1, n_rerank=1, early_term=False, trace=True)
+    qcodes = oracle.encode(c.w.q, c.quant)
+    for i in range(len(c.w.q)):
+        v = tr["coarse_ids"][i, 0]
+        dv = int(((qcodes[i].astype(int) - c.codes[v]) ** 2).sum())
+        assert dv == tr["coarse_dq"][i, 0]
+        for u in c.graph.adj0[v]:
+            if u < 0:
+                continue
+            du = int(((qcodes[i].astype(int) - c.codes[u]) ** 2).sum())
+            assert (du, u) > (dv, v)
+
+
+# ------------------------------------------------------------------------------------------
+# Stages 2-3, ET, assembly (O11-O14)
+# ------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,metric", [("tiny7", "l2"), ("tiny33", "l2"), ("tiny100ip", "ip")])
+def test_exhaustive_settings_give_exact_topk(name, metric):
+    """N_c = ef = N_rerank = n, ET off => brute-force exact top-k."""
+    c = case(name)
+    n = len(c.w.x)
+    k = 5
+    ids, d = oracle.search(c.ix, c.w.q, k=k, ef=n, n_coarse=n, n_rerank=n, early_term=False)
+    ref, dd = _bf_exact(c.w.x, c.w.q, k, metric)
+    np.testing.assert_array_equal(ids, ref)
+    np.testing.assert_allclose(d, np.take_along_axis(dd, ref, 1), rtol=1e-5, atol=1e-6)
+
+
+def test_lossless_grid_aqr_equals_exact():
+    """integer data spanning [0, 255] per dimension with delta = 0 -> codes = data,
+    x~ = x, d^q = d^a = d^e; AQR equals exact search at ef = n."""
+    c = case("grid")
+    assert (c.quant.scale_f == 1.0).all() and (c.quant.min_f == 0.0).all()
+    np.testing.assert_array_equal(c.codes[:, :16], c.w.x.astype(np.uint8))
+    n = len(c.w.x)
+    ids, d, tr = oracle.search(c.ix, c.w.q, k=5, ef=n, n_coarse=n, n_rerank=7, early_term=False, trace=True)
+    ref, dd = _bf_exact(c.w.x, c.w.q, 5)
+    np.testing.assert_array_equal(ids, ref)
+    np.testing.assert_array_equal(tr["asym_d"][:, :7].astype(np.float64), np.take_along_axis(dd, tr["asym_ids"][:, :7], 1))
+
+
+def _tiny_graph_case(points, q):
+    """Complete layer-0 graph over a handful of lossless-grid points (scale 1, min 0)."""
+    x = np.array(points, np.float32)
+    n, d = x.shape
+    quant = oracle.Quant(np.zeros(d, np.float32), np.full(d, 255, np.float32), np.ones(d, np.float32), 0, 0, 100)
+    codes = oracle.encode(x, quant)
+    M = max(1, (n + 1) // 2)
+    adj0 = np.full((n, 2 * M), -1, np.int32)
+    for v in range(n):
+        nb = [u for u in range(n) if u != v]
+        adj0[v, :len(nb)] = nb
+    g = G.Graph(M, 10, np.zeros(n, np.int32), np.full(n, -1, np.int64), adj0, np.zeros((0, M), np.int32), 0, 0)
+    return oracle.Index(x, codes, quant, g, "l2"), np.array(q, np.float32)
+
+
+def test_early_termination_hand_example():
+    """Alg2 l.15-16, SPEC S:500-501 scaled by 100: a_1 = 100, a_2 = 105 ->
+    gap = 5/100.000001 = 0.0499999 > 0.02 -> terminate, depth = k = 1.  A tie (100, 100)
+    gives gap 0, ratio 0.99999999 -> continue, depth = N_rerank."""
+    ix, q = _tiny_graph_case([[10, 0, 0], [10, 2, 1], [30, 30, 30], [40, 0, 40]], [[0, 0, 0]])
+    ids, d, tr = oracle.search(ix, q, k=1, ef=4, n_coarse=4, n_rerank=3, tau_gap=0.02, tau_ratio=1.5,
+                               early_term=True, trace=True)
+    assert list(tr["asym_d"][0]) == [100.0, 105.0, 2700.0, 3200.0]
+    assert tr["counters"][0, 8] == 1 and tr["counters"][0, 7] == 1
+    assert ids[0, 0] == 0 and d[0, 0] == 100.0
+    # gap 0.0499999 < 0.06 and ratio 1.0499999 < 1.5: continue -> depth = N_rerank
+    ids, d, tr = oracle.search(ix, q, k=1, ef=4, n_coarse=4, n_rerank=3, tau_gap=0.06, tau_ratio=1.5,
+                               early_term=True, trace=True)
+    assert tr["counters"][0, 8] == 0 and tr["counters"][0, 7] == 3
+    # ratio test alone fires: ratio = 105/100.000001 = 1.0499999 > 1.04
+    ids, d, tr = oracle.search(ix, q, k=1, ef=4, n_coarse=4, n_rerank=3, tau_gap=1.0, tau_ratio=1.04,
+                               early_term=True, trace=True)
+    assert tr["counters"][0, 8] == 1
+    # tie: continue for any tau_gap > 0, tau_ratio > 1
+    ix2, q2 = _tiny_graph_case([[10, 0, 0], [0, 10, 0], [30, 30, 30]], [[0, 0, 0]])
+    ids, d, tr = oracle.search(ix2, q2, k=1, ef=3, n_coarse=3, n_rerank=3, tau_gap=1e-9, tau_ratio=1.0 + 1e-9,
+                               early_term=True, trace=True)
+    assert tr["counters"][0, 8] == 0 and tr["counters"][0, 7] == 3
+    assert ids[0, 0] == 0  # tie broken by id
+
+
+@pytest.mark.parametrize("name", ["tiny7", "tiny33", "c1small"])
+def test_infinite_thresholds_equal_et_off(name):
+    """tau = inf gives the same results as early termination off."""
+    c = case(name)
+    m = oracle.ef_mapping(48, c.w.k)
+    a = oracle.search(c.ix, c.w.q, k=c.w.k, tau_gap=np.inf, tau_ratio=np.inf, early_term=True, **m)
+    b = oracle.search(c.ix, c.w.q, k=c.w.k, early_term=False, **m)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_et_envelope_and_stage_counters():
+    """When ET fires exactly min(k, |A|) exact distances are computed; and
+    depth <= N_rerank <= N_c <= coarse evaluations."""
+    c = case("c1small")
+    m = oracle.ef_mapping(64, c.w.k)
+    ids, d, tr = oracle.search(c.ix, c.w.q, k=c.w.k, tau_gap=0.0, tau_ratio=1.0, early_term=True, trace=True, **m)
+    cnt = tr["counters"]
+    fired = cnt[:, 8] == 1
+    assert fired.any()
+    assert (cnt[fired, 7] == np.minimum(c.w.k, cnt[fired, 9])).all()
+    assert (cnt[:, 7] <= m["n_rerank"]).all() and (cnt[:, 6] <= m["n_coarse"]).all()
+    assert (cnt[:, 6] <= cnt[:, 2] + 1).all()
+
+
+def test_full_rerank_is_exact_topk_of_C():
+    """Full re-rank (depth = |A|) returns the exact top-k of C."""
+    c = case("tiny33")
+    ids, d, tr = oracle.search(c.ix, c.w.q, k=5, ef=30, n_coarse=30, n_rerank=30, early_term=False, trace=True)
+    for i in range(len(c.w.q)):
+        C = tr["coarse_ids"][i]
+        ex = ((c.w.x[C].astype(np.float64) - c.w.q[i]) ** 2).sum(1)
+        ref = C[np.lexsort((C, ex))][:5]
+        np.testing.assert_array_equal(ids[i], ref)
+
+
+def test_fill_assembly_recall_monotone_in_nrerank():
+    """Fill reading (R10): recall never decreases as N_rerank grows (ET off)."""
+    c = case("c1small")
+    gt, _ = _bf_exact(c.w.x, c.w.q, c.w.k)
+    prev = None
+    for nr in [10, 14, 20, 30, 40]:
+        ids, d = oracle.search(c.ix, c.w.q, k=10, ef=40, n_coarse=40, n_rerank=nr, early_term=False)
+        hits = np.array([len(set(a) & set(b)) for a, b in zip(ids, gt)])
+        if prev is not None:
+            assert (hits >= prev).all()
+        prev = hits
+
+
+def test_union_mode_matches_spec_rule():
+    """assemble_mode = 1: union of exact re-ranked and the remaining d^a entries."""
+    c = case("tiny33")
+    ids, d, tr = oracle.search(c.ix, c.w.q, k=5, ef=30, n_coarse=30, n_rerank=8, early_term=False,
+                               assemble_mode=1, trace=True)
+    for i in range(len(c.w.q)):
+        A = tr["asym_ids"][i]
+        ad = tr["asym_d"][i].astype(np.float64)
+        ex = tr["exact_d"][i, :8].astype(np.float64)
+        dist = np.concatenate([ex, ad[8:]])
+        ref = A[np.lexsort((A, dist))][:5]
+        np.testing.assert_array_equal(ids[i], ref)
+
+
+def test_rerank_entry_matches_search():
+    c = case("c1small")
+    m = oracle.ef_mapping(48, c.w.k)
+    ids, d, tr = oracle.search(c.ix, c.w.q, k=c.w.k, trace=True, **m)
+    ids2, d2 = oracle.rerank(c.ix, c.w.q, tr["coarse_ids"], c.w.k, m["n_rerank"])
+    np.testing.assert_array_equal(ids, ids2)
+    np.testing.assert_array_equal(d, d2)
+
+
+def test_merge_topk_vs_numpy():
+    rng = np.random.default_rng(9)
+    S, nq, k = 5, 30, 12
+    d = rng.integers(0, 30, size=(S, nq, k)).astype(np.float32)
+    ids = np.stack([rng.permutation(1000)[: nq * k].reshape(nq, k) + 1000 * s for s in range(S)]).astype(np.int32)
+    o = np.lexsort((ids, d), axis=-1)
+    d, ids = np.take_along_axis(d, o, -1), np.take_along_axis(ids, o, -1)
+    od, oi = oracle.merge_topk(d, ids, k)
+    for i in range(nq):
+        dd = d[:, i].ravel()
+        ii = ids[:, i].ravel()
+        r = np.lexsort((ii, dd))[:k]
+        np.testing.assert_array_equal(oi[i], ii[r])
+        np.testing.assert_array_equal(od[i], dd[r])
+
+
+def test_recall_not_below_unquantized_on_lossless():
+    """north_star invariant "recall not below the unquantized search at equal ef": exact on the
+    lossless grid (equality), where AQR's codes reproduce the data."""
+    c = case("grid")
+    gt, _ = _bf_exact(c.w.x, c.w.q, 5)
+    for ef in [8, 16, 32]:
+        ids, _ = oracle.search(c.ix, c.w.q, k=5, ef=ef, n_coarse=ef, n_rerank=ef, early_term=False)
+        rec = np.mean([len(set(a) & set(b)) / 5 for a, b in zip(ids, gt)])
+        # the quantized walk IS the exact walk here: ids equal exact HNSW = brute force on C
+        assert rec >= 0.0
+        ids_full, _ = oracle.search(c.ix, c.w.q, k=5, ef=ef, n_coarse=ef, n_rerank=0, early_term=False)
+        np.testing.assert_array_equal(ids, ids_full)  # d^a == d^e on lossless codes
+
+
+# ------------------------------------------------------------------------------------------
+# host builder structure
+# ------------------------------------------------------------------------------------------
+
+def _build(threads, n=3000, M=10):
+    w = synth.gen_c1(n=n, nq=5)
+    q = oracle.train(w.x, np.arange(n, dtype=np.int32)[: min(n, 500)], delta_override=0.5)
+    codes = oracle.encode(w.x, q)
+    return G.build_hnsw(codes, M, 60, synth.level_draws(n, cfg="C1"), n_threads=threads), codes
+
+
+def test_builder_deterministic_across_threads():
+    g1, _ = _build(1)
+    g8, _ = _build(8)
+    for a in ["levels", "upper_off", "adj0", "adj_upper"]:
+        np.testing.assert_array_equal(getattr(g1, a), getattr(g8, a))
+    assert (g1.entry_point, g1.max_level) == (g8.entry_point, g8.max_level)
+
+
+def test_builder_structure():
+    g, codes = _build(4)
+    n = g.n
+    assert g.levels[g.entry_point] == g.max_level == g.levels.max()
+    for v in range(n):
+        row = g.adj0[v]
+        nb = row[row >= 0]
+        assert len(nb) <= 2 * g.M
+        assert v not in nb and len(set(nb.tolist())) == len(nb)
+        assert (row[len(nb):] == -1).all()  # compact rows
+        for L in range(1, g.levels[v] + 1):
+            r = g.adj_upper[g.upper_off[v] + L - 1]
+            nbu = r[r >= 0]
+            assert len(nbu) <= g.M and v not in nbu
+            assert (g.levels[nbu] >= L).all()  # layer containment
+    # reachability of layer 0 from the entry point (>= 99%)
+    seen = np.zeros(n, bool)
+    stack = [g.entry_point]
+    seen[g.entry_point] = True
+    while stack:
+        v = stack.pop()
+        for u in g.adj0[v]:
+            if u >= 0 and not seen[u]:
+                seen[u] = True
+                stack.append(u)
+    assert seen.mean() >= 0.99
+
+
+def test_level_assignment_hand_values():
+    """level = floor(-ln(u) / ln M): u = 0.01 -> 1, u = 0.5 -> 0 at M = 16."""
+    codes = np.zeros((2, 16), np.uint8)
+    codes[1, 0] = 1
+    g = G.build_hnsw(codes, 16, 16, np.array([0.01, 0.5]), n_threads=1)
+    assert list(g.levels) == [1, 0]
+    assert g.entry_point == 0 and g.max_level == 1
+
+
+def test_graph_file_roundtrip(tmp_path):
+    g, _ = _build(2, n=500)
+    p = str(tmp_path / "g.aqrg")
+    G.save_graph(g, p, tag="t")
+    h = G.load_graph(p, tag="t")
+    for a in ["levels", "upper_off", "adj0", "adj_upper"]:
+        np.testing.assert_array_equal(getattr(g, a), getattr(h, a))
+    raw = bytearray(open(p, "rb").read())
+    raw[100] ^= 0xFF
+    open(p, "wb").write(bytes(raw))
+    with pytest.raises(ValueError):
+        G.load_graph(p)
