@@ -36,6 +36,7 @@ EF_GRID = [16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 768, 1024]
 P_MAX = {"C1": 5.0, "C2": 0.2, "C3": 5.0, "C4": 5.0, "C5": 5.0}
 TARGET_RECALL = 0.98
 LAYOUT = "auto"
+BUILD_FLAGS = 1  # host builder: Malkov's keepPrunedConnections (R14)
 
 
 def log(*a):
@@ -184,7 +185,8 @@ def build_index(w, cfg, rank, world, threads):
     M, efc = G.adapt_params(w.M0, w.efc0, quant.delta, eta)
     t1 = time.time()
     if rank == 0:
-        g = G.build_hnsw(codes.cpu().numpy(), M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg=cfg), threads)
+        g = G.build_hnsw(codes.cpu().numpy(), M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg=cfg), threads,
+                         flags=BUILD_FLAGS)
         arrs = [g.levels, g.upper_off, g.adj0, g.adj_upper, np.array([g.entry_point, g.max_level], np.int64)]
     else:
         arrs = [None] * 5
@@ -194,7 +196,7 @@ def build_index(w, cfg, rank, world, threads):
         g = G.Graph(M, efc, arrs[0], arrs[1], arrs[2], arrs[3], int(arrs[4][0]), int(arrs[4][1]))
     t_build = time.time() - t1
     ix = aqr.upload_index(codes, x, quant, g, metric=w.metric, layout=LAYOUT)
-    info = dict(layout=ix.layout, delta=quant.delta, eta=eta, M=M, efc=efc, p_max=P_MAX[cfg], p_low=quant.p_low, p_high=quant.p_high,
+    info = dict(layout=ix.layout, build_flags=BUILD_FLAGS, delta=quant.delta, eta=eta, M=M, efc=efc, p_max=P_MAX[cfg], p_low=quant.p_low, p_high=quant.p_high,
                 encode_s=round(t_enc, 2), build_s=round(t_build, 2), max_level=g.max_level,
                 index_bytes=ix.device_bytes())
     return x, codes, quant, g, ix, info
@@ -454,7 +456,8 @@ def run_reference(args):
     codes = oracle.encode(w.x, quant)
     eta = G.eta_of(G.density_weights(w.x[sample], rho))
     M, efc = G.adapt_params(w.M0, w.efc0, quant.delta, eta)
-    g = G.build_hnsw(codes, M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg=cfg), args.threads)
+    g = G.build_hnsw(codes, M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg=cfg), args.threads,
+                     flags=BUILD_FLAGS)
     log(f"[reference] index built in {time.time() - t0:.1f} s")
     ef = 256 if args.ef == "auto" else int(args.ef)
     m = G_ef_mapping(ef, k)

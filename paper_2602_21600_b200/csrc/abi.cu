@@ -264,8 +264,8 @@ static aqr_status check_search_params(const aqr_search_params* p, bool need_ef) 
   AQR_CHECK_ARG(p->tau_gap >= 0.0, "search: tau_gap must be >= 0");
   AQR_CHECK_ARG(p->tau_ratio >= 1.0, "search: tau_ratio must be >= 1");
   AQR_CHECK_ARG(p->assemble_mode == 0 || p->assemble_mode == 1, "search: assemble_mode must be 0 or 1");
-  AQR_CHECK_ARG(p->visited_bits == 0 || (p->visited_bits >= 6 && p->visited_bits <= 16),
-                "search: visited_bits must be 0 or in [6, 16]");
+  AQR_CHECK_ARG(p->visited_bits == 0 || p->visited_bits == -1 || (p->visited_bits >= 6 && p->visited_bits <= 16),
+                "search: visited_bits must be 0 (auto), -1 (no visited hash) or in [6, 16]");
   AQR_CHECK_ARG(p->warps_per_block >= 0 && p->warps_per_block <= 8, "search: warps_per_block must be in [0, 8]");
   return AQR_OK;
 }
@@ -280,7 +280,7 @@ static aqr::SearchCfg make_cfg(const aqr_search_params* p) {
   c.tau_ratio = p->tau_ratio;
   c.early_term = p->early_term;
   c.assemble_mode = p->assemble_mode;
-  c.hbits = p->visited_bits ? p->visited_bits : auto_hbits(p->ef);
+  c.hbits = p->visited_bits > 0 ? p->visited_bits : (p->visited_bits < 0 ? 0 : auto_hbits(p->ef));
   return c;
 }
 

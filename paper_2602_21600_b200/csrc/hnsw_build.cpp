@@ -106,8 +106,10 @@ std::vector<Key> search_layer(const Graph& g, int64_t q, const std::vector<Key>&
 
 // Malkov's neighbour-selection heuristic: scan candidates ascending by distance to the base
 // point; keep e unless some already kept r is strictly closer to e than the base is.
-std::vector<int32_t> heuristic(const Graph& g, const std::vector<Key>& cand_sorted, int32_t m) {
-  std::vector<int32_t> sel;
+// keep_pruned (Malkov's keepPrunedConnections option): fill the remaining slots with the
+// closest discarded candidates.
+std::vector<int32_t> heuristic(const Graph& g, const std::vector<Key>& cand_sorted, int32_t m, bool keep_pruned) {
+  std::vector<int32_t> sel, pruned;
   sel.reserve(m);
   for (const Key& e : cand_sorted) {
     if ((int32_t)sel.size() >= m) break;
@@ -116,7 +118,9 @@ std::vector<int32_t> heuristic(const Graph& g, const std::vector<Key>& cand_sort
       if (g.dist(e.second, r) < e.first) { good = false; break; }
     }
     if (good) sel.push_back(e.second);
+    else if (keep_pruned) pruned.push_back(e.second);
   }
+  for (size_t i = 0; i < pruned.size() && (int32_t)sel.size() < m; ++i) sel.push_back(pruned[i]);
   return sel;
 }
 
@@ -175,7 +179,10 @@ int64_t aqr_hnsw_levels(const double* u, int64_t n, int32_t M, int32_t* levels, 
 // pos / batch_div nodes (0 = 32; a huge value gives sequential insertion).  Returns 0 on success.
 int aqr_hnsw_build(const uint8_t* codes, int64_t n, int32_t d_pad, const int32_t* levels,
                    const int64_t* upper_off, int32_t M, int32_t efc, int32_t n_threads,
-                   int32_t* adj0, int32_t* adj_upper, int64_t upper_rows, int32_t* out2, int32_t batch_div) {
+                   int32_t* adj0, int32_t* adj_upper, int64_t upper_rows, int32_t* out2, int32_t batch_div, int32_t flags) {
+  // flags bit 0: keep pruned connections; bit 1: a new node selects 2M (not M) layer-0 neighbours
+  const bool keep_pruned = (flags & 1) != 0;
+  const int32_t sel0 = (flags & 2) ? 2 * M : M;
   if (!codes || n < 1 || M < 2 || efc < 1 || !adj0 || !out2) return 1;
   Graph g;
   g.n = n; g.d_pad = d_pad; g.M = M; g.cap0 = 2 * M; g.efc = efc; g.codes = codes;
@@ -227,7 +234,7 @@ int aqr_hnsw_build(const uint8_t* codes, int64_t n, int32_t d_pad, const int32_t
       std::vector<Key> eps{Key(dcur, cur)};
       for (int32_t L = std::min(lq, g.max_level); L >= 0; --L) {
         std::vector<Key> W = search_layer(g, q, eps, efc, L, s);
-        std::vector<int32_t> nb = heuristic(g, W, M);
+        std::vector<int32_t> nb = heuristic(g, W, L == 0 ? sel0 : M, keep_pruned);
         int32_t* r = g.row(q, L);
         for (size_t t = 0; t < nb.size(); ++t) r[t] = nb[t];
         sel[bi].emplace_back(L, std::move(nb));
@@ -260,7 +267,7 @@ int aqr_hnsw_build(const uint8_t* codes, int64_t n, int32_t d_pad, const int32_t
       for (int32_t t = 0; t < deg; ++t) cand.emplace_back(g.dist(e, r[t]), r[t]);
       for (int64_t i = a; i < b; ++i) cand.emplace_back(g.dist(e, rev[i].src), rev[i].src);
       std::sort(cand.begin(), cand.end());
-      std::vector<int32_t> nb = heuristic(g, cand, cp);
+      std::vector<int32_t> nb = heuristic(g, cand, cp, keep_pruned);
       for (int32_t t = 0; t < cp; ++t) r[t] = t < (int32_t)nb.size() ? nb[t] : -1;
     });
     for (int64_t bi = 0; bi < B; ++bi)

@@ -52,10 +52,6 @@ __device__ __forceinline__ uint64_t akey(float d, int32_t id) {
   return ((uint64_t)fkey(d) << 32) | (uint32_t)id;
 }
 
-__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
-  uint32_t lo = __shfl_sync(kFull, (uint32_t)v, src), hi = __shfl_sync(kFull, (uint32_t)(v >> 32), src);
-  return ((uint64_t)hi << 32) | lo;
-}
 __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
   uint32_t lo = __shfl_xor_sync(kFull, (uint32_t)v, m), hi = __shfl_xor_sync(kFull, (uint32_t)(v >> 32), m);
   return ((uint64_t)hi << 32) | lo;
@@ -105,17 +101,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// number of keys in sorted a[0:n) strictly less than key
-__device__ __forceinline__ int lower_bound_u64(const uint64_t* a, int n, uint64_t key) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (a[mid] < key) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-// same, ignoring the expanded flag bit of W entries
+// number of W keys strictly less than key, ignoring the expanded flag bit
 __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t key) {
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -130,7 +116,7 @@ __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t 
 // per-warp shared-memory layout
 // ------------------------------------------------------------------------------------
 struct Layout {
-  int o_qc, o_qf, o_w, o_h, o_nb, o_nd, o_cand, o_cs, o_bar, per_warp;
+  int o_qc, o_qf, o_w, o_h, o_nb, o_nd, o_cand, o_cs, o_lb, o_bar, per_warp;
   int region;     // bytes of the hash / block-buffer region (reused by Stage 2/3)
   int buf_bytes;  // INLINE: one staged block (128-byte aligned)
 };
@@ -144,7 +130,7 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c) {
   L.o_qf = o; o += al16(4 * ix.d4);
   L.o_w = o; o += al16(8 * (c.ef + 1));
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
-  int hb = ix.blk ? 2 * L.buf_bytes : (4 << c.hbits);
+  int hb = ix.blk ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
   int s23 = 20 * c.n_coarse + 32;
   L.region = hb > s23 ? hb : s23;
   o = (o + 127) & ~127;
@@ -153,6 +139,7 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c) {
   L.o_nd = o; o += al16(4 * ix.ld0);
   L.o_cand = o; o += al16(8 * ix.ld0);
   L.o_cs = o; o += al16(8 * ix.ld0);
+  L.o_lb = o; o += al16(4 * ix.ld0);
   L.o_bar = o; o += 16;
   L.per_warp = (o + 127) & ~127;
   return L;
@@ -478,15 +465,16 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
   uint64_t* cand = reinterpret_cast<uint64_t*>(wb + L.o_cand);
   uint64_t* cs = reinterpret_cast<uint64_t*>(wb + L.o_cs);
   uint64_t* bar = reinterpret_cast<uint64_t*>(wb + L.o_bar);
-  uint8_t* bufs[2] = {wb + L.o_h, wb + L.o_h + L.buf_bytes};
+  int32_t* clb = reinterpret_cast<int32_t*>(wb + L.o_lb);
+  uint8_t* blkbuf = wb + L.o_h;
+  uint32_t* vhash = c.hbits > 0 ? hash : nullptr;
   const int sub = lane % LPR;
   const int nch = ix.d_pad >> 4;
   const int ef = c.ef;
-  uint32_t phase[2] = {0u, 0u};
+  uint32_t phase = 0u;
   if (INL) {
     if (lane == 0) {
       mbar_init(bar, 1);
-      mbar_init(bar + 1, 1);
       fence_proxy_async();
     }
     __syncwarp();
@@ -547,21 +535,22 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
     }
 
     // 3. layer-0 beam (flag form)
-    int b = 0;
     if (INL) {
       if (lane == 0) {
         fence_proxy_async();
-        bulk_load(bufs[0], ix.blk + (int64_t)cur * ix.blk_stride, (uint32_t)ix.blk_bytes, bar);
+        bulk_load(blkbuf, ix.blk + (int64_t)cur * ix.blk_stride, (uint32_t)ix.blk_bytes, bar);
         W[0] = qkey(dcur, cur);
       }
     } else {
-      uint4* h4 = reinterpret_cast<uint4*>(hash);
-      const int nh4 = (1 << c.hbits) >> 2;
-      for (int t = lane; t < nh4; t += 32) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+      if (vhash) {
+        uint4* h4 = reinterpret_cast<uint4*>(hash);
+        const int nh4 = (1 << c.hbits) >> 2;
+        for (int t = lane; t < nh4; t += 32) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+      }
       __syncwarp();
       if (lane == 0) {
         W[0] = qkey(dcur, cur);
-        visit_new(hash, c.hbits, cur, fails);
+        if (vhash) visit_new(hash, c.hbits, cur, fails);
       }
     }
     __syncwarp();
@@ -587,20 +576,26 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
       int m;
       const int32_t* ids;
       if (INL) {
-        // the block of cnode was bulk-copied into bufs[b] (prefetched)
-        mbar_wait(bar + b, phase[b]);
-        phase[b] ^= 1u;
-        ids = reinterpret_cast<const int32_t*>(bufs[b]);
+        // the block of cnode was bulk-copied into blkbuf (prefetched during the last merge);
+        // its ids are copied out so the buffer can take the next block before the merge
+        mbar_wait(bar, phase);
+        phase ^= 1u;
         m = ix.cap0;
         int deg = 0;
-        for (int t0 = 0; t0 < m; t0 += 32) deg += __popc(__ballot_sync(kFull, t0 + lane < m && ids[t0 + lane] >= 0));
+        for (int t0 = 0; t0 < m; t0 += 32) {
+          const int32_t u = t0 + lane < m ? reinterpret_cast<const int32_t*>(blkbuf)[t0 + lane] : -1;
+          if (t0 + lane < m) nb[t0 + lane] = u;
+          deg += __popc(__ballot_sync(kFull, u >= 0));
+        }
+        ids = nb;
         cnt[1] += deg;
         cnt[2] += deg;
-        block_dists<LPR, CPL>(bufs[b] + ix.blk_ids, ix.d_pad, qreg, qq, ids, m, nd, lane);
+        block_dists<LPR, CPL>(blkbuf + ix.blk_ids, ix.d_pad, qreg, qq, reinterpret_cast<const int32_t*>(blkbuf), m,
+                              nd, lane);
       } else {
         // neighbours not yet visited
         int deg;
-        m = gather_row(ix.adj0 + (int64_t)cnode * ix.ld0, ix.cap0, nb, hash, c.hbits, fails, deg, lane);
+        m = gather_row(ix.adj0 + (int64_t)cnode * ix.ld0, ix.cap0, nb, vhash, c.hbits, fails, deg, lane);
         ids = nb;
         cnt[1] += deg;
         cnt[2] += m;
@@ -615,20 +610,23 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
         const int r = r0 + lane;
         bool ok = false;
         uint64_t kk = 0;
+        int lb = 0;
         if (r < m) {
           const int32_t id = ids[r];
           if (id >= 0) {
             kk = qkey((uint32_t)nd[r], id);
             ok = kk < maxk;
             if (ok) {
-              const int lb = lower_bound_w(W, size, kk);
+              lb = lower_bound_w(W, size, kk);
               ok = !(lb < size && (W[lb] & ~1ull) == kk);
             }
           }
         }
         const uint32_t mk = __ballot_sync(kFull, ok);
         if (ok) {
-          cand[np + __popc(mk & ((1u << lane) - 1u))] = kk;
+          const int j = np + __popc(mk & ((1u << lane) - 1u));
+          cand[j] = kk;
+          clb[j] = lb;
           cmin = kk < cmin ? kk : cmin;
         }
         np += __popc(mk);
@@ -651,26 +649,26 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
         __syncwarp();
         if (nxt != ~0ull && lane == 0) {
           fence_proxy_async();
-          bulk_load(bufs[b ^ 1], ix.blk + (int64_t)qkey_id(nxt) * ix.blk_stride, (uint32_t)ix.blk_bytes,
-                    bar + (b ^ 1));
+          bulk_load(blkbuf, ix.blk + (int64_t)qkey_id(nxt) * ix.blk_stride, (uint32_t)ix.blk_bytes, bar);
         }
-        b ^= 1;
       }
       __syncwarp();
       if (np == 0) {
         cursor = pos + 1;
         continue;
       }
-      // merge: candidate final slot = (#W keys below) + (rank among candidates)
-      rank_sort(cand, cs, np, lane);
-      int first_ins = size;
+      // merge: sorted candidate r lands at slb[r] + r (slb = #W keys below it, from the filter);
+      // an old entry W[i] moves right by #{r : slb[r] <= i}
+      int32_t* slb = reinterpret_cast<int32_t*>(nd);
       for (int i = lane; i < np; i += 32) {
-        const int lb = lower_bound_w(W, size, cs[i]);
-        nd[i] = lb + i;  // nd reused as the candidate destinations
-        if (i == 0) first_ins = lb;
+        const uint64_t kk = cand[i];
+        int r = 0;
+        for (int j = 0; j < np; ++j) r += cand[j] < kk;
+        cs[r] = kk;
+        slb[r] = clb[i];
       }
-      first_ins = __shfl_sync(kFull, first_ins, 0);
       __syncwarp();
+      const int first_ins = slb[0];
       // shift the old entries W[first_ins:size) right, top chunk first (in place)
       for (int hi = size; hi > first_ins; hi -= 32) {
         const int lo = hi - 32 > first_ins ? hi - 32 : first_ins;
@@ -679,14 +677,18 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
         int dst = INT_MAX;
         if (i < hi) {
           v = W[i];
-          dst = i + lower_bound_u64(cs, np, v & ~1ull);
+          int sh = 0;
+          for (int j = 0; j < np; ++j) sh += slb[j] <= i;
+          dst = i + sh;
         }
         __syncwarp();
         if (i < hi && dst < ef) W[dst] = v;
         __syncwarp();
       }
-      for (int i = lane; i < np; i += 32)
-        if (nd[i] < ef) W[nd[i]] = cs[i];
+      for (int i = lane; i < np; i += 32) {
+        const int dst = slb[i] + i;
+        if (dst < ef) W[dst] = cs[i];
+      }
       __syncwarp();
       size = size + np < ef ? size + np : ef;
       cursor = first_ins < pos + 1 ? first_ins : pos + 1;
@@ -697,6 +699,7 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
     // debug: C with d^q
     const int nc = c.n_coarse < size ? c.n_coarse : size;
     int32_t* cid = reinterpret_cast<int32_t*>(wb + L.o_h);
+    (void)cs;
     uint64_t* akeys = reinterpret_cast<uint64_t*>(wb + L.o_h + al16(4 * nc));
     uint64_t* rkeys = akeys + nc;
     __syncwarp();
@@ -751,7 +754,7 @@ __global__ void __launch_bounds__(128) rerank_kernel(IndexView ix, SearchCfg c, 
                                                      int64_t nq, int64_t ld_q, const int32_t* __restrict__ cand,
                                                      int32_t n_cand, int32_t* __restrict__ out_ids,
                                                      float* __restrict__ out_dist, int per_warp, int o_reg) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int64_t qi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (qi >= nq) return;

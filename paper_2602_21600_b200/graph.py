@@ -45,7 +45,7 @@ class Graph:
 
 
 def build_hnsw(codes: np.ndarray, M: int, efc: int, level_u: np.ndarray, n_threads: int = 0,
-               batch_div: int = 0) -> Graph:
+               batch_div: int = 0, flags: int = 0) -> Graph:
     """Deterministic batched HNSW insert over u8 codes [n, d_pad] (Alg1 l.16-22)."""
     codes = np.ascontiguousarray(codes, dtype=np.uint8)
     n, d_pad = codes.shape
@@ -62,7 +62,7 @@ def build_hnsw(codes: np.ndarray, M: int, efc: int, level_u: np.ndarray, n_threa
                           levels.ctypes.data_as(C.c_void_p), upper_off.ctypes.data_as(C.c_void_p), C.c_int32(M),
                           C.c_int32(efc), C.c_int32(n_threads), adj0.ctypes.data_as(C.c_void_p),
                           adj_upper.ctypes.data_as(C.c_void_p) if rows > 0 else None, C.c_int64(rows),
-                          out2.ctypes.data_as(C.c_void_p), C.c_int32(batch_div))
+                          out2.ctypes.data_as(C.c_void_p), C.c_int32(batch_div), C.c_int32(flags))
     if st != 0:
         raise RuntimeError(f"aqr_hnsw_build failed ({st})")
     return Graph(M, efc, levels, upper_off, adj0, adj_upper, int(out2[0]), int(out2[1]))
