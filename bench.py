@@ -30,7 +30,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-EF_GRID = [16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 768, 1024]
+EF_GRID = [16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 640, 768, 896, 1024, 1280, 1536]
 # per-config quantizer window P_max (never given by the paper; R4) and the
 # fixed HNSW construction inputs of BASELINE.json
 P_MAX = {"C1": 5.0, "C2": 0.2, "C3": 5.0, "C4": 5.0, "C5": 5.0}
@@ -202,15 +202,38 @@ def build_index(w, cfg, rank, world, threads):
     return x, codes, quant, g, ix, info
 
 
-def bytes_per_query(tot, nq, d, k):
+def bytes_per_query(tot, nq, d, k, distinct_ratio=1.0):
     """Algorithmic bytes from the kernel counters:
-    query 4d + adjacency 4(deg+1) per expansion (all layers) + d per distinct code evaluation
-    (all layers; re-evaluations after a visited-hash miss excluded) + N_c d (Stage 2 re-read)
-    + 4d per exact re-rank + 8k output."""
+    query 4d + adjacency 4(deg+1) per expansion (all layers) + d per DISTINCT code evaluation
+    (all layers) + N_c d (Stage 2 re-read) + 4d per exact re-rank + 8k output.  The kernel
+    counts every neighbour it scores (it keeps no exact visited set); `distinct_ratio` = distinct
+    evaluations / neighbours scored, measured exactly by the oracle (same visit order) on a query
+    sample, converts that count to the algorithmic one."""
     exp, deg, ev, uexp, udeg, uev, nc, depth, et, na, fails = [float(v) for v in tot]
-    b = (4 * d * nq + 4 * (deg + exp) + 4 * (udeg + uexp) + d * (ev - fails + uev) + d * nc + 4 * d * depth
-         + 8 * k * nq)
+    b = (4 * d * nq + 4 * (deg + exp) + 4 * (udeg + uexp) + d * ((ev - fails) * distinct_ratio + uev) + d * nc
+         + 4 * d * depth + 8 * k * nq)
     return b / nq
+
+
+def oracle_index(w, cfg, codes, g):
+    """The oracle trains its own quantizer and encodes the base itself (full-size parity check
+    of aqr_encode: codes compared byte for byte), then searches the same graph."""
+    import oracle
+    import synth
+    t0 = time.time()
+    sample = synth.density_sample(len(w.x), seed=w.seed, cfg=cfg)
+    o_quant = oracle.train(w.x, sample, p_max=P_MAX[cfg])
+    o_codes = oracle.encode(w.x, o_quant)
+    codes_equal = bool(np.array_equal(o_codes, codes.cpu().numpy()))
+    return oracle.Index(w.x, o_codes, o_quant, g, w.metric), codes_equal, time.time() - t0
+
+
+def distinct_ratio_from_oracle(oix, w, m, k, n_sample=256):
+    import oracle
+    _, _, tr = oracle.search(oix, w.q[:n_sample], k, trace=True, exp_cap=1, **m)
+    cnt = tr["counters"].sum(0)
+    # layer-0 distinct evaluations / layer-0 neighbours seen (oracle counters 2 and 1)
+    return float(cnt[2]) / max(float(cnt[1]), 1.0), int(len(w.q[:n_sample]))
 
 
 # --------------------------------------------------------------------------------------------
@@ -242,7 +265,7 @@ def run_aqr(args):
     grid = EF_GRID if args.ef == "auto" else [int(args.ef)]
     for ef in grid:
         m = aqr.ef_mapping(ef, k)
-        p = aqr.make_params(k, **m)
+        p = aqr.make_params(k, **m, visited_bits=args.vbits[0])
         s = aqr.Searcher(ix, len(q), p)
         s.run(q)
         torch.cuda.synchronize()
@@ -295,7 +318,13 @@ def run_aqr(args):
     s.run(q, stats=True)
     torch.cuda.synchronize()
     tot_counters = s.totals.cpu().numpy()
-    bq = bytes_per_query(tot_counters, len(q), w.x.shape[1], k)
+    oix, codes_equal, t_otrain = (None, None, 0.0)
+    ratio, n_ratio = 1.0, 0
+    if rank == 0 and not args.no_oracle:
+        oix, codes_equal, t_otrain = oracle_index(w, cfg, codes, g)
+        ratio, n_ratio = distinct_ratio_from_oracle(oix, w, m, k)
+    ratio = float(allreduce_sum([ratio if rank == 0 else 0.0], world)[0]) if world > 1 else ratio
+    bq = bytes_per_query(tot_counters, len(q), w.x.shape[1], k, ratio)
 
     # ---- device-timed region: W warm-up steps, then K steps bracketed by barrier + sync ----
     stream = torch.cuda.current_stream()
@@ -373,8 +402,10 @@ def run_aqr(args):
 
     # ---- CPU oracle baseline: rank 0, N = 1, bounded query sample ----
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(w, cfg, quant, codes, g, m, k, args.cpu_seconds, s)
+    if rank == 0 and world == 1 and not args.no_cpu and oix is not None:
+        cpu = cpu_baseline(w, oix, m, k, args.cpu_seconds, s)
+        cpu["codes_equal_full_size"] = codes_equal
+        cpu["oracle_train_s"] = round(t_otrain, 1)
 
     if rank == 0:
         line = {
@@ -391,6 +422,7 @@ def run_aqr(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "bytes_per_query": round(bq, 1), "peak_source": peak_src,
+                         "distinct_eval_ratio": round(ratio, 4), "distinct_ratio_sample": n_ratio,
                          "kernel": "search_kernel", "kernel_ms": round(launch_ms, 4)},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_val, 1), "unit": "queries/s",
@@ -407,19 +439,9 @@ def run_aqr(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(w, cfg, quant, codes, g, m, k, seconds, searcher):
-    """The CPU oracle as it stands, single thread, on a bounded sample of the same queries.
-    The oracle trains its own quantizer and encodes the base itself; the codes are compared
-    byte for byte with the GPU's (full-size parity) before the oracle searches the same graph."""
+def cpu_baseline(w, oix, m, k, seconds, searcher):
+    """The CPU oracle as it stands, single thread, on a bounded sample of the same queries."""
     import oracle
-    import synth
-    t0 = time.time()
-    sample = synth.density_sample(len(w.x), seed=w.seed, cfg=cfg)
-    o_quant = oracle.train(w.x, sample, p_max=P_MAX[cfg])
-    o_codes = oracle.encode(w.x, o_quant)
-    codes_equal = bool(np.array_equal(o_codes, codes.cpu().numpy()))
-    t_train = time.time() - t0
-    oix = oracle.Index(w.x, o_codes, o_quant, g, w.metric)
     n_try = 8
     t0 = time.time()
     oracle.search(oix, w.q[:n_try], k, **m)
@@ -431,7 +453,6 @@ def cpu_baseline(w, cfg, quant, codes, g, m, k, seconds, searcher):
     g_ids = searcher.ids[:n_s].cpu().numpy()
     return {"value": round(n_s / el, 2), "unit": "queries/s", "cores": 1, "kind": "oracle",
             "sample": f"first {n_s} of {len(w.q)} queries, same graph/ef ({el:.1f} s single-threaded C oracle)",
-            "codes_equal_full_size": codes_equal, "oracle_train_s": round(t_train, 1),
             "ids_equal_frac": round(float((o_ids == g_ids).all(1).mean()), 4)}
 
 
@@ -502,11 +523,12 @@ def main():
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--ef", default="auto")
     ap.add_argument("--full-sweep", action="store_true")
-    ap.add_argument("--vbits", type=lambda v: [int(t) for t in v.split(",")], default=[0],
+    ap.add_argument("--vbits", type=lambda v: [int(t) for t in v.split(",")], default=[-1],
                     help="visited-hash sizes (log2 slots, 0 = auto) tried at the chosen ef; fastest is timed")
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-oracle", action="store_true", help="skip the oracle index (no cpu_baseline, ratio 1)")
     ap.add_argument("--split", dest="weak", action="store_false",
                     help="split one query batch across ranks instead of every rank searching all queries")
     ap.add_argument("--layout", default="auto", choices=["auto", "gather", "inline"])

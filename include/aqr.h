@@ -148,9 +148,9 @@ typedef struct {
   double tau_ratio;     /* >= 1 */
   int32_t early_term;   /* 1 = apply the early-termination test (Alg2 l.15-16) */
   int32_t assemble_mode;/* 0 = fill (R10, default), 1 = union */
-  int32_t visited_bits; /* GATHER layout: log2 of the per-query visited-hash slots in shared memory
-                           (0 = auto, -1 = no visited set: re-encountered nodes are re-scored and
-                           dropped by the W dedupe, R15).  INLINE layout: ignored (no hash). */
+  int32_t visited_bits; /* GATHER layout: log2 of the per-query visited-hash slots in shared memory,
+                           6..16; 0 or -1 = no visited set (default): re-encountered nodes are
+                           re-scored and dropped by the W dedupe (R15).  INLINE: ignored. */
   int32_t warps_per_block; /* 0 = auto */
 } aqr_search_params;
 

@@ -46,13 +46,6 @@ aqr_status cuda_fail(cudaError_t e, const char* where) {
 
 int32_t round_up(int32_t x, int32_t m) { return (x + m - 1) / m * m; }
 
-int auto_hbits(int ef) {
-  // visited-hash slots ~ 16 x ef, between 2^10 and 2^13
-  int b = 10;
-  while (b < 13 && (1 << b) < 16 * ef) ++b;
-  return b;
-}
-
 }  // namespace
 
 extern "C" {
@@ -280,7 +273,7 @@ static aqr::SearchCfg make_cfg(const aqr_search_params* p) {
   c.tau_ratio = p->tau_ratio;
   c.early_term = p->early_term;
   c.assemble_mode = p->assemble_mode;
-  c.hbits = p->visited_bits > 0 ? p->visited_bits : (p->visited_bits < 0 ? 0 : auto_hbits(p->ef));
+  c.hbits = p->visited_bits > 0 ? p->visited_bits : 0;
   return c;
 }
 

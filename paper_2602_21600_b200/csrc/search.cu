@@ -116,7 +116,7 @@ __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t 
 // per-warp shared-memory layout
 // ------------------------------------------------------------------------------------
 struct Layout {
-  int o_qc, o_qf, o_w, o_h, o_nb, o_nd, o_cand, o_cs, o_lb, o_bar, per_warp;
+  int o_qc, o_qf, o_w, o_h, o_s23, o_nb, o_nd, o_cand, o_cs, o_lb, o_bar, per_warp;
   int region;     // bytes of the hash / block-buffer region (reused by Stage 2/3)
   int buf_bytes;  // INLINE: one staged block (128-byte aligned)
 };
@@ -130,11 +130,10 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c) {
   L.o_qf = o; o += al16(4 * ix.d4);
   L.o_w = o; o += al16(8 * (c.ef + 1));
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
-  int hb = ix.blk ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
-  int s23 = 20 * c.n_coarse + 32;
-  L.region = hb > s23 ? hb : s23;
+  L.region = ix.blk ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
   o = (o + 127) & ~127;
   L.o_h = o; o += al16(L.region);
+  L.o_s23 = o; o += c.ef >= 2 * c.n_coarse ? 0 : al16(8 * c.n_coarse);
   L.o_nb = o; o += al16(4 * ix.ld0);
   L.o_nd = o; o += al16(4 * ix.ld0);
   L.o_cand = o; o += al16(8 * ix.ld0);
@@ -312,13 +311,17 @@ __device__ __forceinline__ float exact_row(const IndexView& ix, const float* qf,
 // Stages 2 / ET / 3 / assembly for one query (Alg2 l.8-24).  cid[0:nc] in smem holds C in
 // (d^q, id) order; region holds >= 20*nc bytes of scratch after cid.
 // ------------------------------------------------------------------------------------
-__device__ void finish_query(const IndexView& ix, const SearchCfg& c, const float* qf, int32_t* cid, int nc,
-                             uint64_t* akeys, uint64_t* rkeys, int64_t qi, int32_t* out_ids, float* out_dist,
-                             const aqr_debug& dbg, bool has_dbg, int lane, int64_t* cnt) {
+// C comes either as ids (cid) or as the first nc W keys (wk, which may alias rkeys: entry i is
+// read before it is overwritten).  akeys / rkeys: nc 64-bit keys each.
+__device__ void finish_query(const IndexView& ix, const SearchCfg& c, const float* qf, const int32_t* cid,
+                             const uint64_t* wk, int nc, uint64_t* akeys, uint64_t* rkeys, int64_t qi,
+                             int32_t* out_ids, float* out_dist, const aqr_debug& dbg, bool has_dbg, int lane,
+                             int64_t* cnt) {
   // Stage 2: d^a for every entry of C (Alg2 l.10-12)
   for (int i = 0; i < nc; ++i) {
-    const int32_t id = cid[i];
+    const int32_t id = cid ? cid[i] : qkey_id(wk[i]);
     const float da = asym_row(ix, qf, id, lane);
+    __syncwarp();
     if (lane == 0) rkeys[i] = akey(da, id);
   }
   __syncwarp();
@@ -698,28 +701,21 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
 
     // debug: C with d^q
     const int nc = c.n_coarse < size ? c.n_coarse : size;
-    int32_t* cid = reinterpret_cast<int32_t*>(wb + L.o_h);
-    (void)cs;
-    uint64_t* akeys = reinterpret_cast<uint64_t*>(wb + L.o_h + al16(4 * nc));
-    uint64_t* rkeys = akeys + nc;
     __syncwarp();
-    for (int i = lane; i < nc; i += 32) {
-      const uint64_t wkk = W[i];
-      cid[i] = qkey_id(wkk);
-      if (has_dbg) {
-        if (dbg.coarse_ids) dbg.coarse_ids[qi * c.n_coarse + i] = qkey_id(wkk);
-        if (dbg.coarse_dq) dbg.coarse_dq[qi * c.n_coarse + i] = (int32_t)qkey_d(wkk);
-      }
-    }
     if (has_dbg) {
-      for (int i = nc + lane; i < c.n_coarse; i += 32) {
-        if (dbg.coarse_ids) dbg.coarse_ids[qi * c.n_coarse + i] = -1;
-        if (dbg.coarse_dq) dbg.coarse_dq[qi * c.n_coarse + i] = -1;
+      for (int i = lane; i < c.n_coarse; i += 32) {
+        const uint64_t wkk = i < nc ? W[i] : 0;
+        if (dbg.coarse_ids) dbg.coarse_ids[qi * c.n_coarse + i] = i < nc ? qkey_id(wkk) : -1;
+        if (dbg.coarse_dq) dbg.coarse_dq[qi * c.n_coarse + i] = i < nc ? (int32_t)qkey_d(wkk) : -1;
       }
     }
+    // Stage 2/3 scratch lives in W: unsorted keys overwrite W[0:nc] in place, A goes to
+    // W[nc:2nc] (ef >= 2 N_c, as with m_ef >= 2), else to a separate area
+    uint64_t* akeys = ef >= 2 * nc ? W + nc : reinterpret_cast<uint64_t*>(wb + L.o_s23);
+    uint64_t* rkeys = W;
     __syncwarp();
     // 4-7. Stage 2, early termination, Stage 3, assembly
-    finish_query(ix, c, qf, cid, nc, akeys, rkeys, qi, out_ids, out_dist, dbg, has_dbg != 0, lane, cnt);
+    finish_query(ix, c, qf, nullptr, W, nc, akeys, rkeys, qi, out_ids, out_dist, dbg, has_dbg != 0, lane, cnt);
     if (has_dbg && lane == 0) {
       if (dbg.counters)
         for (int t = 0; t < AQR_NCOUNT; ++t) dbg.counters[qi * AQR_NCOUNT + t] = cnt[t];
@@ -777,7 +773,7 @@ __global__ void __launch_bounds__(128) rerank_kernel(IndexView ix, SearchCfg c, 
   aqr_debug none{};
   SearchCfg cc = c;
   cc.n_coarse = n_cand;
-  finish_query(ix, cc, qf, cid, nc, akeys, rkeys, qi, out_ids, out_dist, none, false, lane, nullptr);
+  finish_query(ix, cc, qf, cid, nullptr, nc, akeys, rkeys, qi, out_ids, out_dist, none, false, lane, nullptr);
 }
 
 template <int LPR, int CPL, bool INL>
