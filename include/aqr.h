@@ -100,7 +100,7 @@ typedef struct {
   int64_t ld_base;           /* >= d */
   const float *min_j;        /* device [d] trained quantizer (aqr_quant_params) */
   const float *scale_j;      /* device [d] */
-  int32_t M;                 /* degree cap at layers >= 1; layer-0 rows hold 2*M entries */
+  int32_t M;                 /* degree cap at layers >= 1 (1..80); layer-0 rows hold 2*M entries */
   int32_t max_level;         /* top layer */
   int32_t entry_point;       /* a node of level max_level */
   const int32_t *adj0;       /* host [n x 2M], -1 padded, ids in [0, n) */

@@ -116,7 +116,7 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   AQR_CHECK_ARG(D.metric == AQR_L2 || D.metric == AQR_IP, "upload: bad metric");
   AQR_CHECK_ARG(D.codes && D.base && D.min_j && D.scale_j && D.adj0 && D.upper_off, "upload: null array");
   AQR_CHECK_ARG(D.ld_base >= D.d, "upload: ld_base < d");
-  AQR_CHECK_ARG(D.M >= 1 && 2 * D.M <= 1024, "upload: need 1 <= M <= 512");
+  AQR_CHECK_ARG(D.M >= 1 && D.M <= 80, "upload: need 1 <= M <= 80 (layer-0 rows of <= 160 entries)");
   AQR_CHECK_ARG(D.max_level >= 0 && D.max_level <= 64, "upload: bad max_level");
   AQR_CHECK_ARG(D.entry_point >= 0 && D.entry_point < D.n, "upload: entry_point out of range");
   AQR_CHECK_ARG(D.upper_rows >= 0 && (D.upper_rows == 0 || D.adj_upper), "upload: adj_upper missing");

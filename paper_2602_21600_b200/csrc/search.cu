@@ -152,7 +152,9 @@ template <int LPR, int CPL>
 __device__ __forceinline__ void list_dists(const IndexView& ix, const uint4 (&qreg)[CPL], int qq,
                                            const int32_t* ids, int m, int32_t* out, int lane) {
   constexpr int G = 32 / LPR;
-  constexpr int U = CPL == 1 ? 8 : (CPL == 2 ? 4 : 2);
+  // all loads of a pass are issued before any is consumed: 16 / CPL rows per lane group, so a
+  // typical layer-0 expansion (<= 64 rows of 128 B) costs ONE DRAM round trip
+  constexpr int U = 16 / CPL;
   const int g = lane / LPR, sub = lane % LPR;
   const int nch = ix.d_pad >> 4;
   for (int r0 = 0; r0 < m; r0 += G * U) {
@@ -557,6 +559,18 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
       }
     }
     __syncwarp();
+    // GATHER: the layer-0 row of the node to expand next is held in registers (lane owns entries
+    // lane + 32 t); it is loaded for the entry point here and, afterwards, prefetched for the next
+    // expansion right after the filter so the load overlaps the merge
+    constexpr int kRowRegs = 5;  // cap0 = 2M <= 160 (ABI: M <= 80)
+    int32_t arow[kRowRegs];
+    if (!INL) {
+#pragma unroll
+      for (int t = 0; t < kRowRegs; ++t) {
+        const int j = lane + 32 * t;
+        arow[t] = j < ix.cap0 ? __ldg(ix.adj0 + (int64_t)cur * ix.ld0 + j) : -1;
+      }
+    }
     int size = 1, cursor = 0, nexp = 0;
     for (;;) {
       // smallest unexpanded entry of W
@@ -596,9 +610,20 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
         block_dists<LPR, CPL>(blkbuf + ix.blk_ids, ix.d_pad, qreg, qq, reinterpret_cast<const int32_t*>(blkbuf), m,
                               nd, lane);
       } else {
-        // neighbours not yet visited
-        int deg;
-        m = gather_row(ix.adj0 + (int64_t)cnode * ix.ld0, ix.cap0, nb, vhash, c.hbits, fails, deg, lane);
+        // neighbours (not yet visited, when the optional hash is on) from the prefetched row
+        int deg = 0;
+        m = 0;
+#pragma unroll
+        for (int t = 0; t < kRowRegs; ++t) {
+          const int32_t u = arow[t];
+          deg += __popc(__ballot_sync(kFull, u >= 0));
+          bool keep = u >= 0;
+          if (keep && vhash) keep = visit_new(hash, c.hbits, u, fails);
+          const uint32_t mk = __ballot_sync(kFull, keep);
+          if (keep) nb[m + __popc(mk & ((1u << lane) - 1u))] = u;
+          m += __popc(mk);
+        }
+        __syncwarp();
         ids = nb;
         cnt[1] += deg;
         cnt[2] += m;
@@ -634,9 +659,10 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
         }
         np += __popc(mk);
       }
-      if (INL) {
+      {
         // the next expansion is min(first unexpanded entry of W after pos, smallest candidate);
-        // start its bulk copy now so it overlaps the merge (prefetch only, never speculative)
+        // start loading its layer-0 data now so the load overlaps the merge (prefetch only,
+        // never speculative: this node IS expanded next)
         cmin = warp_min_u64(cmin);
         uint64_t kw = ~0ull;
         for (int bb = pos + 1; bb < size; bb += 32) {
@@ -650,9 +676,18 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
         }
         const uint64_t nxt = kw < cmin ? kw : cmin;
         __syncwarp();
-        if (nxt != ~0ull && lane == 0) {
-          fence_proxy_async();
-          bulk_load(blkbuf, ix.blk + (int64_t)qkey_id(nxt) * ix.blk_stride, (uint32_t)ix.blk_bytes, bar);
+        if (INL) {
+          if (nxt != ~0ull && lane == 0) {
+            fence_proxy_async();
+            bulk_load(blkbuf, ix.blk + (int64_t)qkey_id(nxt) * ix.blk_stride, (uint32_t)ix.blk_bytes, bar);
+          }
+        } else if (nxt != ~0ull) {
+          const int64_t rb = (int64_t)qkey_id(nxt) * ix.ld0;
+#pragma unroll
+          for (int t = 0; t < kRowRegs; ++t) {
+            const int j = lane + 32 * t;
+            arow[t] = j < ix.cap0 ? __ldg(ix.adj0 + rb + j) : -1;
+          }
         }
       }
       __syncwarp();
