@@ -151,7 +151,7 @@ typedef struct {
   int32_t visited_bits; /* GATHER layout: log2 of the per-query visited-hash slots in shared memory,
                            6..16; 0 or -1 = no visited set (default): re-encountered nodes are
                            re-scored and dropped by the W dedupe (R15).  INLINE: ignored. */
-  int32_t warps_per_block; /* 0 = auto */
+  int32_t warps_per_block; /* reserved, must be 0 (the CTA shape is fixed at compile time) */
 } aqr_search_params;
 
 #define AQR_NCOUNT 11

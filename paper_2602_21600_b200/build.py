@@ -45,6 +45,23 @@ def build_aqr(force=False, verbose=False):
     return LIB_AQR
 
 
+def build_variant(name: str, defines: dict, force=False):
+    """Build libaqr_<name>.so with -D overrides of the compile-time tuning knobs (tools/perf.py)."""
+    out = os.path.join(PKG, f"libaqr_{name}.so")
+    srcs = [os.path.join(CSRC, s) for s in CU_SOURCES]
+    deps = srcs + [os.path.join(CSRC, "aqr_internal.cuh"), os.path.join(ROOT, "include", "aqr.h")]
+    if force or _stale(out, deps):
+        flags = [f for f in NVCC_FLAGS if f not in ("-Xptxas", "-v")]
+        cmd = [NVCC, *flags, *[f"-D{k}={v}" for k, v in defines.items()], "-I", os.path.join(ROOT, "include"),
+               *srcs, "-o", out + ".tmp"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed building {out}")
+        os.replace(out + ".tmp", out)
+    return out
+
+
 def build_hnsw(force=False):
     src = os.path.join(CSRC, "hnsw_build.cpp")
     if force or _stale(LIB_HNSW, [src]):

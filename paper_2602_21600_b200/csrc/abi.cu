@@ -291,12 +291,11 @@ aqr_status aqr_search(const aqr_index* ix, const float* q, int64_t nq, int64_t l
   AQR_CHECK_ARG(ws != nullptr && ws_bytes >= 256, "search: workspace too small");
   AQR_CHECK_ARG(!debug || !debug->exp_ids || debug->exp_cap >= 1, "search: debug exp_cap < 1");
   aqr::SearchCfg c = make_cfg(p);
-  int wpb = p->warps_per_block ? p->warps_per_block : 4;
+#ifndef AQR_WARPS_PER_CTA
+#define AQR_WARPS_PER_CTA 4
+#endif
+  int wpb = AQR_WARPS_PER_CTA;
   size_t smem = aqr::search_smem_bytes(ix->v, c, wpb);
-  while (smem > 227 * 1024 && wpb > 1) {
-    --wpb;
-    smem = aqr::search_smem_bytes(ix->v, c, wpb);
-  }
   if (smem > 227 * 1024) {
     set_error("aqr: search: per-warp shared memory exceeds 227 KB (reduce ef or visited_bits)");
     return AQR_E_UNSUPPORTED;

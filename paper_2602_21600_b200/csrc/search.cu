@@ -28,6 +28,20 @@ namespace aqr {
 
 namespace {
 
+// tuning knobs (compile-time; tools/perf.py A/B-tests variants built with -D overrides)
+#ifndef AQR_WARPS_PER_CTA
+#define AQR_WARPS_PER_CTA 4
+#endif
+#ifndef AQR_MIN_CTAS
+#define AQR_MIN_CTAS 5  // 5 CTAs x 4 warps: the shared-memory limit at ef ~ 900 (<= 102 regs)
+#endif
+#ifndef AQR_ROWS_PER_PASS
+#define AQR_ROWS_PER_PASS 16  // 16-byte code chunks in flight per lane per gather pass
+#endif
+#ifndef AQR_PREFETCH_ROW
+#define AQR_PREFETCH_ROW 1
+#endif
+
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kProbes = 8;
@@ -145,6 +159,36 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c) {
 }
 
 // ------------------------------------------------------------------------------------
+// Transpose reduction of U per-lane partial sums over groups of LPR lanes (LPR, U powers of 2).
+// Step with offset o (o = LPR/2 .. 1) halves the live partials: lanes with (sub & o) keep the
+// upper half of their rows, the others the lower half, each adding its partner's copy.  At the
+// end (U >= LPR) lane `sub` holds, in part[0 .. U/LPR), the totals of rows sub*(U/LPR) + v.
+// If U < LPR the last log2(LPR/U) steps are plain butterflies on a single value.
+// ------------------------------------------------------------------------------------
+template <int LPR, int U>
+__device__ __forceinline__ void reduce_rows(int (&part)[U], int sub) {
+  int n = U;  // live partials
+#pragma unroll
+  for (int o = LPR / 2; o >= 1; o >>= 1) {
+    if (n > 1) {
+      const int h = n / 2;
+      const bool upper = (sub & o) != 0;
+#pragma unroll
+      for (int v = 0; v < U / 2; ++v) {
+        if (v < h) {
+          const int send = upper ? part[v] : part[v + h];
+          const int keep = upper ? part[v + h] : part[v];
+          part[v] = keep + __shfl_xor_sync(kFull, send, o);
+        }
+      }
+      n = h;
+    } else {
+      part[0] += __shfl_xor_sync(kFull, part[0], o);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // d^q for a list of node ids: LPR lanes per code row, CPL 16-byte chunks per lane
 // d^q = sum q^2 + sum x^2 - 2 sum q x  (exact int32; dp4a on u8x4 words)
 // ------------------------------------------------------------------------------------
@@ -154,7 +198,7 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const uint4 (&qr
   constexpr int G = 32 / LPR;
   // all loads of a pass are issued before any is consumed: 16 / CPL rows per lane group, so a
   // typical layer-0 expansion (<= 64 rows of 128 B) costs ONE DRAM round trip
-  constexpr int U = 16 / CPL;
+  constexpr int U = AQR_ROWS_PER_PASS / CPL;
   const int g = lane / LPR, sub = lane % LPR;
   const int nch = ix.d_pad >> 4;
   for (int r0 = 0; r0 < m; r0 += G * U) {
@@ -170,6 +214,7 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const uint4 (&qr
         buf[u][t] = (id >= 0 && c < nch) ? ldg_stream(row + c) : make_uint4(0, 0, 0, 0);
       }
     }
+    int part[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       unsigned xx = 0, qx = 0;
@@ -181,11 +226,19 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const uint4 (&qr
         xx = __dp4a(w.z, w.z, xx); qx = __dp4a(qw.z, w.z, qx);
         xx = __dp4a(w.w, w.w, xx); qx = __dp4a(qw.w, w.w, qx);
       }
-      int s = (int)xx - 2 * (int)qx;
+      part[u] = (int)xx - 2 * (int)qx;
+    }
+    // transpose-reduce across the LPR lanes of a row group (U/2 + U/4 + ... shuffles instead of
+    // U * log2(LPR)); afterwards lane `sub` holds the total of row u = sub * PER + v in part[v]
+    // (U >= LPR), or, when U < LPR, every lane holds the total of row sub / (LPR / U)
+    reduce_rows<LPR, U>(part, sub);
+    constexpr int PER = U >= LPR ? U / LPR : 1;
+    constexpr int REP = U >= LPR ? 1 : LPR / U;
 #pragma unroll
-      for (int off = LPR / 2; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+    for (int v = 0; v < PER; ++v) {
+      const int u = U >= LPR ? sub * PER + v : sub / REP;
       const int r = r0 + u * G + g;
-      if (sub == 0 && r < m) out[r] = qq + s;
+      if ((sub % REP) == 0 && r < m) out[r] = qq + part[v];
     }
   }
 }
@@ -428,6 +481,7 @@ __device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, c
         buf[u][t] = (id >= 0 && c < nch) ? row[c] : make_uint4(0, 0, 0, 0);
       }
     }
+    int part[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       unsigned xx = 0, qx = 0;
@@ -439,11 +493,19 @@ __device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, c
         xx = __dp4a(w.z, w.z, xx); qx = __dp4a(qw.z, w.z, qx);
         xx = __dp4a(w.w, w.w, xx); qx = __dp4a(qw.w, w.w, qx);
       }
-      int s = (int)xx - 2 * (int)qx;
+      part[u] = (int)xx - 2 * (int)qx;
+    }
+    // transpose-reduce across the LPR lanes of a row group (U/2 + U/4 + ... shuffles instead of
+    // U * log2(LPR)); afterwards lane `sub` holds the total of row u = sub * PER + v in part[v]
+    // (U >= LPR), or, when U < LPR, every lane holds the total of row sub / (LPR / U)
+    reduce_rows<LPR, U>(part, sub);
+    constexpr int PER = U >= LPR ? U / LPR : 1;
+    constexpr int REP = U >= LPR ? 1 : LPR / U;
 #pragma unroll
-      for (int off = LPR / 2; off; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+    for (int v = 0; v < PER; ++v) {
+      const int u = U >= LPR ? sub * PER + v : sub / REP;
       const int r = r0 + u * G + g;
-      if (sub == 0 && r < m) out[r] = qq + s;
+      if ((sub % REP) == 0 && r < m) out[r] = qq + part[v];
     }
   }
 }
@@ -454,7 +516,7 @@ __device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, c
 // shared-memory visited hash)
 // ------------------------------------------------------------------------------------
 template <int LPR, int CPL, bool INL>
-__global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, Layout L, const float* __restrict__ q,
+__global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_kernel(IndexView ix, SearchCfg c, Layout L, const float* __restrict__ q,
                                                      int64_t nq, int64_t ld_q, int32_t* __restrict__ out_ids,
                                                      float* __restrict__ out_dist, aqr_debug dbg, int has_dbg,
                                                      int* __restrict__ counter) {
@@ -611,6 +673,13 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
                               nd, lane);
       } else {
         // neighbours (not yet visited, when the optional hash is on) from the prefetched row
+        if (!AQR_PREFETCH_ROW) {
+#pragma unroll
+          for (int t = 0; t < kRowRegs; ++t) {
+            const int j = lane + 32 * t;
+            arow[t] = j < ix.cap0 ? __ldg(ix.adj0 + (int64_t)cnode * ix.ld0 + j) : -1;
+          }
+        }
         int deg = 0;
         m = 0;
 #pragma unroll
@@ -681,7 +750,7 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
             fence_proxy_async();
             bulk_load(blkbuf, ix.blk + (int64_t)qkey_id(nxt) * ix.blk_stride, (uint32_t)ix.blk_bytes, bar);
           }
-        } else if (nxt != ~0ull) {
+        } else if (AQR_PREFETCH_ROW && nxt != ~0ull) {
           const int64_t rb = (int64_t)qkey_id(nxt) * ix.ld0;
 #pragma unroll
           for (int t = 0; t < kRowRegs; ++t) {
@@ -715,9 +784,14 @@ __global__ void __launch_bounds__(256) search_kernel(IndexView ix, SearchCfg c, 
         int dst = INT_MAX;
         if (i < hi) {
           v = W[i];
-          int sh = 0;
-          for (int j = 0; j < np; ++j) sh += slb[j] <= i;
-          dst = i + sh;
+          // #{r : slb[r] <= i} by binary search (slb is non-decreasing)
+          int a = 0, z = np;
+          while (a < z) {
+            const int mid = (a + z) >> 1;
+            if (slb[mid] <= i) a = mid + 1;
+            else z = mid;
+          }
+          dst = i + a;
         }
         __syncwarp();
         if (i < hi && dst < ef) W[dst] = v;
