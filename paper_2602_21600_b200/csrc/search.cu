@@ -699,31 +699,42 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         list_dists<LPR, CPL>(ix, qreg, qq, nb, m, nd, lane);
       }
       __syncwarp();
-      // filter against max W (when full) and drop re-evaluations already in W (R15)
+      // filter against max W (when full), then drop re-evaluations already in W (R15): the
+      // survivors of the cheap key test are compacted first so the W binary search (which also
+      // yields each candidate's insertion rank) runs once per survivor, not once per neighbour
       const uint64_t maxk = size >= ef ? (W[size - 1] & ~1ull) : ~0ull;
-      int np = 0;
-      uint64_t cmin = ~0ull;
+      int np0 = 0;
       for (int r0 = 0; r0 < m; r0 += 32) {
         const int r = r0 + lane;
         bool ok = false;
         uint64_t kk = 0;
-        int lb = 0;
         if (r < m) {
           const int32_t id = ids[r];
-          if (id >= 0) {
-            kk = qkey((uint32_t)nd[r], id);
-            ok = kk < maxk;
-            if (ok) {
-              lb = lower_bound_w(W, size, kk);
-              ok = !(lb < size && (W[lb] & ~1ull) == kk);
-            }
-          }
+          kk = qkey((uint32_t)nd[r], id);
+          ok = id >= 0 && kk < maxk;
+        }
+        const uint32_t mk = __ballot_sync(kFull, ok);
+        if (ok) cs[np0 + __popc(mk & ((1u << lane) - 1u))] = kk;
+        np0 += __popc(mk);
+      }
+      __syncwarp();
+      int np = 0;
+      uint64_t cmin = ~0ull;
+      for (int j0 = 0; j0 < np0; j0 += 32) {
+        const int j = j0 + lane;
+        bool ok = false;
+        uint64_t kk = 0;
+        int lb = 0;
+        if (j < np0) {
+          kk = cs[j];
+          lb = lower_bound_w(W, size, kk);
+          ok = !(lb < size && (W[lb] & ~1ull) == kk);
         }
         const uint32_t mk = __ballot_sync(kFull, ok);
         if (ok) {
-          const int j = np + __popc(mk & ((1u << lane) - 1u));
-          cand[j] = kk;
-          clb[j] = lb;
+          const int jj = np + __popc(mk & ((1u << lane) - 1u));
+          cand[jj] = kk;
+          clb[jj] = lb;
           cmin = kk < cmin ? kk : cmin;
         }
         np += __popc(mk);
@@ -776,25 +787,21 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       }
       __syncwarp();
       const int first_ins = slb[0];
-      // shift the old entries W[first_ins:size) right, top chunk first (in place)
+      // shift the old entries W[first_ins:size) right, top chunk first (in place).  Entry i moves
+      // by sh(i) = #{r : slb[r] <= i}; walking down, r_hi tracks #{r : slb[r] <= hi - 1} and only
+      // the few candidates whose slb falls inside the chunk adjust individual lanes, so the whole
+      // shift costs O(chunks + np) uniform steps instead of a search per entry
+      int r_hi = np;
       for (int hi = size; hi > first_ins; hi -= 32) {
         const int lo = hi - 32 > first_ins ? hi - 32 : first_ins;
+        while (r_hi > 0 && slb[r_hi - 1] > hi - 1) --r_hi;
         const int i = lo + lane;
+        int sh = r_hi;
+        for (int r = r_hi; r > 0 && slb[r - 1] > lo; --r) sh -= slb[r - 1] > i;
         uint64_t v = 0;
-        int dst = INT_MAX;
-        if (i < hi) {
-          v = W[i];
-          // #{r : slb[r] <= i} by binary search (slb is non-decreasing)
-          int a = 0, z = np;
-          while (a < z) {
-            const int mid = (a + z) >> 1;
-            if (slb[mid] <= i) a = mid + 1;
-            else z = mid;
-          }
-          dst = i + a;
-        }
+        if (i < hi) v = W[i];
         __syncwarp();
-        if (i < hi && dst < ef) W[dst] = v;
+        if (i < hi && i + sh < ef) W[i + sh] = v;
         __syncwarp();
       }
       for (int i = lane; i < np; i += 32) {
