@@ -263,7 +263,8 @@ def run_aqr(args):
     sweep = []
     chosen = None
     grid = EF_GRID if args.ef == "auto" else [int(args.ef)]
-    for ef in grid:
+
+    def measure(ef):
         m = aqr.ef_mapping(ef, k)
         p = aqr.make_params(k, **m, visited_bits=args.vbits[0])
         s = aqr.Searcher(ix, len(q), p)
@@ -279,16 +280,39 @@ def run_aqr(args):
         ed = E.exact_dist(x, q, ids, w.metric).cpu().numpy()
         ov, ta = E.recall(ids.cpu().numpy(), gt_ids, ed, gt_d, k)
         tot = allreduce_sum([ov * len(q), ta * len(q), len(q)], world)
-        ov_all, ta_all = tot[0] / tot[2], tot[1] / tot[2]
         ms_max = allreduce_max(ms, world)
-        sweep.append(dict(ef=ef, n_coarse=m["n_coarse"], n_rerank=m["n_rerank"], recall=round(ta_all, 4),
-                          recall_id=round(ov_all, 4), qps=round(float(tot[2]) / (ms_max / 1e3), 1)))
+        r = dict(ef=ef, n_coarse=m["n_coarse"], n_rerank=m["n_rerank"], recall=round(tot[1] / tot[2], 4),
+                 recall_id=round(tot[0] / tot[2], 4), qps=round(float(tot[2]) / (ms_max / 1e3), 1))
         if rank == 0:
-            log(f"[bench] sweep {sweep[-1]}")
-        if ta_all >= TARGET_RECALL and chosen is None:
+            log(f"[bench] sweep {r}")
+        return r
+
+    prev = None
+    for ef in grid:
+        r = measure(ef)
+        sweep.append(r)
+        if r["recall"] >= TARGET_RECALL and chosen is None:
             chosen = ef
             if args.ef == "auto" and not args.full_sweep:
                 break
+        if chosen is None:
+            prev = ef
+    if chosen is not None and prev is not None and args.ef == "auto":
+        # refine: the smallest ef (multiple of 16) between the last failing grid point and the first
+        # passing one whose recall@10 >= target (recall is monotone in ef up to noise; bisection)
+        lo, hi = prev, chosen
+        while hi - lo > 16:
+            mid = (lo + hi) // 2 // 16 * 16
+            if mid <= lo:
+                break
+            r = measure(mid)
+            sweep.append(r)
+            if r["recall"] >= TARGET_RECALL:
+                hi = mid
+            else:
+                lo = mid
+        chosen = hi
+    sweep.sort(key=lambda z: z["ef"])
     if chosen is None:
         chosen = grid[-1]
     m = aqr.ef_mapping(chosen, k)

@@ -118,23 +118,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// number of W keys strictly less than key, ignoring the expanded flag bit
-__device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t key) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if ((a[mid] & ~1ull) < key) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
 // ------------------------------------------------------------------------------------
 // per-warp shared-memory layout
 // ------------------------------------------------------------------------------------
 struct Layout {
   int o_qc, o_qf, o_w, o_h, o_s23, o_nb, o_nd, o_cand, o_cs, o_lb, o_bar, per_warp;
-  int region;     // bytes of the hash / block-buffer region (reused by Stage 2/3)
+  int region;     // bytes of the hash / block-buffer region
+  int wcap;       // W ring capacity (slots)
   int buf_bytes;  // INLINE: one staged block (128-byte aligned)
 };
 
@@ -145,12 +135,13 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c) {
   int o = 0;
   L.o_qc = o; o += al16(ix.d_pad);
   L.o_qf = o; o += al16(4 * ix.d4);
-  L.o_w = o; o += al16(8 * (c.ef + 1));
+  L.wcap = c.ef + ix.ld0;  // W ring slots (see the beam): ef + one layer-0 row of headroom
+  L.o_w = o; o += al16(8 * L.wcap);
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
   L.region = ix.blk ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
   o = (o + 127) & ~127;
   L.o_h = o; o += al16(L.region);
-  L.o_s23 = o; o += c.ef >= 2 * c.n_coarse ? 0 : al16(8 * c.n_coarse);
+  L.o_s23 = o; o += (c.n_coarse > 32 * kLinRegs || L.wcap < 2 * c.n_coarse) ? al16(8 * c.n_coarse) : 0;
   L.o_nb = o; o += al16(4 * ix.ld0);
   L.o_nd = o; o += al16(4 * ix.ld0);
   L.o_cand = o; o += al16(8 * ix.ld0);
@@ -637,22 +628,31 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = __ldg(ix.adj0 + (int64_t)cur * ix.ld0 + j);
       }
     }
+    // W is a ring of wcap slots holding the sorted list in DESCENDING order: logical (ascending)
+    // index i lives in slot (tail - 1 - i) mod wcap.  New candidates land near the logical front
+    // (they are close to the query), so only the few entries in front of the last insertion point
+    // move; the entries behind it keep their slots (tail advances by np) and evicting the largest
+    // entries is free (they simply fall out of the logical range [0, ef)).
+    const int wcap = L.wcap;
+    int tail = 1;
+    auto slot = [&](int i, int t) { const int p = t - 1 - i; return p < 0 ? p + wcap : p; };
     int size = 1, cursor = 0, nexp = 0;
     for (;;) {
       // smallest unexpanded entry of W
       int pos = -1;
       for (int bb = cursor; bb < size; bb += 32) {
         const int i = bb + lane;
-        const bool un = i < size && !(W[i] & 1ull);
+        const bool un = i < size && !(W[slot(i, tail)] & 1ull);
         const uint32_t mk = __ballot_sync(kFull, un);
         if (mk) { pos = bb + __ffs(mk) - 1; break; }
       }
       if (pos < 0) break;
-      const uint64_t wk = W[pos];
+      const int pslot = slot(pos, tail);
+      const uint64_t wk = W[pslot];
       const int32_t cnode = qkey_id(wk);
       __syncwarp();
       if (lane == 0) {
-        W[pos] = wk | 1ull;
+        W[pslot] = wk | 1ull;
         if (has_dbg && dbg.exp_ids && nexp < dbg.exp_cap) dbg.exp_ids[qi * dbg.exp_cap + nexp] = cnode;
       }
       ++nexp;
@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       // filter against max W (when full), then drop re-evaluations already in W (R15): the
       // survivors of the cheap key test are compacted first so the W binary search (which also
       // yields each candidate's insertion rank) runs once per survivor, not once per neighbour
-      const uint64_t maxk = size >= ef ? (W[size - 1] & ~1ull) : ~0ull;
+      const uint64_t maxk = size >= ef ? (W[slot(size - 1, tail)] & ~1ull) : ~0ull;
       int np0 = 0;
       for (int r0 = 0; r0 < m; r0 += 32) {
         const int r = r0 + lane;
@@ -733,8 +733,16 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         int lb = 0;
         if (j < np0) {
           kk = cs[j];
-          lb = lower_bound_w(W, size, kk);
-          ok = !(lb < size && (W[lb] & ~1ull) == kk);
+          {  // lower bound of kk in logical [0, size)
+            int a = 0, z = size;
+            while (a < z) {
+              const int mid = (a + z) >> 1;
+              if ((W[slot(mid, tail)] & ~1ull) < kk) a = mid + 1;
+              else z = mid;
+            }
+            lb = a;
+          }
+          ok = !(lb < size && (W[slot(lb, tail)] & ~1ull) == kk);
         }
         const uint32_t mk = __ballot_sync(kFull, ok);
         if (ok) {
@@ -753,10 +761,10 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         uint64_t kw = ~0ull;
         for (int bb = pos + 1; bb < size; bb += 32) {
           const int i = bb + lane;
-          const bool un = i < size && !(W[i] & 1ull);
+          const bool un = i < size && !(W[slot(i, tail)] & 1ull);
           const uint32_t mk = __ballot_sync(kFull, un);
           if (mk) {
-            kw = W[bb + __ffs(mk) - 1];
+            kw = W[slot(bb + __ffs(mk) - 1, tail)];
             break;
           }
         }
@@ -794,27 +802,30 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       }
       __syncwarp();
       const int first_ins = slb[0];
-      // shift the old entries W[first_ins:size) right, top chunk first (in place).  Entry i moves
-      // by sh(i) = #{r : slb[r] <= i}; walking down, r_hi tracks #{r : slb[r] <= hi - 1} and only
-      // the few candidates whose slb falls inside the chunk adjust individual lanes, so the whole
-      // shift costs O(chunks + np) uniform steps instead of a search per entry
-      int r_hi = np;
-      for (int hi = size; hi > first_ins; hi -= 32) {
-        const int lo = hi - 32 > first_ins ? hi - 32 : first_ins;
-        while (r_hi > 0 && slb[r_hi - 1] > hi - 1) --r_hi;
-        const int i = lo + lane;
-        int sh = r_hi;
-        for (int r = r_hi; r > 0 && slb[r - 1] > lo; --r) sh -= slb[r - 1] > i;
+      // entries in front of the last insertion point (logical i < slb[np-1]) move to logical
+      // i + sh(i), sh(i) = #{r : slb[r] <= i}; with tail' = tail + np the entries behind it keep
+      // their slots.  Moves go to higher slots, so chunks are processed from logical 0 upward.
+      const int last = slb[np - 1];
+      int ntail = tail + np;
+      if (ntail >= wcap) ntail -= wcap;
+      int r_lo = 0;
+      for (int i0 = 0; i0 < last; i0 += 32) {
+        const int i1 = i0 + 32 < last ? i0 + 32 : last;
+        while (r_lo < np && slb[r_lo] <= i0) ++r_lo;
+        const int i = i0 + lane;
+        int sh = r_lo;
+        for (int r = r_lo; r < np && slb[r] <= i1 - 1; ++r) sh += slb[r] <= i;
         uint64_t v = 0;
-        if (i < hi) v = W[i];
+        if (i < i1) v = W[slot(i, tail)];
         __syncwarp();
-        if (i < hi && i + sh < ef) W[i + sh] = v;
+        if (i < i1 && i + sh < ef) W[slot(i + sh, ntail)] = v;
         __syncwarp();
       }
       for (int i = lane; i < np; i += 32) {
         const int dst = slb[i] + i;
-        if (dst < ef) W[dst] = cs[i];
+        if (dst < ef) W[slot(dst, ntail)] = cs[i];
       }
+      tail = ntail;
       __syncwarp();
       size = size + np < ef ? size + np : ef;
       cursor = first_ins < pos + 1 ? first_ins : pos + 1;
@@ -822,23 +833,44 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     cnt[0] = nexp;
     cnt[10] = fails;
 
-    // debug: C with d^q
+    // C = the first nc logical entries of W, linearized (ascending) for Stage 2/3: through
+    // registers into W[0:nc) when it fits (the rest of the ring is free scratch), else copied
+    // to the separate s23 area
     const int nc = c.n_coarse < size ? c.n_coarse : size;
+    __syncwarp();
+    uint64_t* lin;
+    uint64_t* akeys;
+    if (nc <= 32 * kLinRegs) {
+      uint64_t tmp[kLinRegs];
+#pragma unroll
+      for (int j = 0; j < kLinRegs; ++j) {
+        const int i = lane + 32 * j;
+        tmp[j] = i < nc ? W[slot(i, tail)] : 0ull;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < kLinRegs; ++j) {
+        const int i = lane + 32 * j;
+        if (i < nc) W[i] = tmp[j];
+      }
+      lin = W;
+      akeys = wcap >= 2 * nc ? W + nc : reinterpret_cast<uint64_t*>(wb + L.o_s23);
+    } else {
+      lin = reinterpret_cast<uint64_t*>(wb + L.o_s23);
+      for (int i = lane; i < nc; i += 32) lin[i] = W[slot(i, tail)];
+      akeys = W;
+    }
     __syncwarp();
     if (has_dbg) {
       for (int i = lane; i < c.n_coarse; i += 32) {
-        const uint64_t wkk = i < nc ? W[i] : 0;
+        const uint64_t wkk = i < nc ? lin[i] : 0;
         if (dbg.coarse_ids) dbg.coarse_ids[qi * c.n_coarse + i] = i < nc ? qkey_id(wkk) : -1;
         if (dbg.coarse_dq) dbg.coarse_dq[qi * c.n_coarse + i] = i < nc ? (int32_t)qkey_d(wkk) : -1;
       }
     }
-    // Stage 2/3 scratch lives in W: unsorted keys overwrite W[0:nc] in place, A goes to
-    // W[nc:2nc] (ef >= 2 N_c, as with m_ef >= 2), else to a separate area
-    uint64_t* akeys = ef >= 2 * nc ? W + nc : reinterpret_cast<uint64_t*>(wb + L.o_s23);
-    uint64_t* rkeys = W;
     __syncwarp();
-    // 4-7. Stage 2, early termination, Stage 3, assembly
-    finish_query(ix, c, qf, nullptr, W, nc, akeys, rkeys, qi, out_ids, out_dist, dbg, has_dbg != 0, lane, cnt);
+    // 4-7. Stage 2, early termination, Stage 3, assembly (unsorted keys overwrite lin in place)
+    finish_query(ix, c, qf, nullptr, lin, nc, akeys, lin, qi, out_ids, out_dist, dbg, has_dbg != 0, lane, cnt);
     if (has_dbg && lane == 0) {
       if (dbg.counters)
         for (int t = 0; t < AQR_NCOUNT; ++t) dbg.counters[qi * AQR_NCOUNT + t] = cnt[t];
