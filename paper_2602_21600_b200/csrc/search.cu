@@ -118,6 +118,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+constexpr int kLinRegs = 12;  // C of up to 32 x 12 entries is linearized through registers
+
 // ------------------------------------------------------------------------------------
 // per-warp shared-memory layout
 // ------------------------------------------------------------------------------------
@@ -802,24 +804,45 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       }
       __syncwarp();
       const int first_ins = slb[0];
-      // entries in front of the last insertion point (logical i < slb[np-1]) move to logical
-      // i + sh(i), sh(i) = #{r : slb[r] <= i}; with tail' = tail + np the entries behind it keep
-      // their slots.  Moves go to higher slots, so chunks are processed from logical 0 upward.
+      // Old entry i moves to logical i + sh(i), sh(i) = #{r : slb[r] <= i}.  The ring lets either
+      // end stay in place (a deque): keep the front fixed (tail unchanged) and move the entries at
+      // or behind the first insertion point (size - first_ins entries), or keep the back fixed
+      // (tail += np) and move the entries in front of the last insertion point (slb[np-1]
+      // entries) -- whichever moves fewer.  Entries whose new position is >= ef are evicted.
       const int last = slb[np - 1];
-      int ntail = tail + np;
-      if (ntail >= wcap) ntail -= wcap;
-      int r_lo = 0;
-      for (int i0 = 0; i0 < last; i0 += 32) {
-        const int i1 = i0 + 32 < last ? i0 + 32 : last;
-        while (r_lo < np && slb[r_lo] <= i0) ++r_lo;
-        const int i = i0 + lane;
-        int sh = r_lo;
-        for (int r = r_lo; r < np && slb[r] <= i1 - 1; ++r) sh += slb[r] <= i;
-        uint64_t v = 0;
-        if (i < i1) v = W[slot(i, tail)];
-        __syncwarp();
-        if (i < i1 && i + sh < ef) W[slot(i + sh, ntail)] = v;
-        __syncwarp();
+      int ntail = tail;
+      if (size - first_ins <= last) {
+        // front fixed: moves go to LOWER slots, so walk from the logical top down
+        int r_hi = np;
+        for (int hi = size; hi > first_ins; hi -= 32) {
+          const int lo = hi - 32 > first_ins ? hi - 32 : first_ins;
+          while (r_hi > 0 && slb[r_hi - 1] > hi - 1) --r_hi;
+          const int i = lo + lane;
+          int sh = r_hi;
+          for (int r = r_hi; r > 0 && slb[r - 1] > lo; --r) sh -= slb[r - 1] > i;
+          uint64_t v = 0;
+          if (i < hi) v = W[slot(i, tail)];
+          __syncwarp();
+          if (i < hi && i + sh < ef) W[slot(i + sh, tail)] = v;
+          __syncwarp();
+        }
+      } else {
+        // back fixed: moves go to HIGHER slots, so walk from logical 0 up
+        ntail = tail + np;
+        if (ntail >= wcap) ntail -= wcap;
+        int r_lo = 0;
+        for (int i0 = 0; i0 < last; i0 += 32) {
+          const int i1 = i0 + 32 < last ? i0 + 32 : last;
+          while (r_lo < np && slb[r_lo] <= i0) ++r_lo;
+          const int i = i0 + lane;
+          int sh = r_lo;
+          for (int r = r_lo; r < np && slb[r] <= i1 - 1; ++r) sh += slb[r] <= i;
+          uint64_t v = 0;
+          if (i < i1) v = W[slot(i, tail)];
+          __syncwarp();
+          if (i < i1 && i + sh < ef) W[slot(i + sh, ntail)] = v;
+          __syncwarp();
+        }
       }
       for (int i = lane; i < np; i += 32) {
         const int dst = slb[i] + i;
