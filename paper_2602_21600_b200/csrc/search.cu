@@ -38,9 +38,6 @@ namespace {
 #ifndef AQR_ROWS_PER_PASS
 #define AQR_ROWS_PER_PASS 16  // 16-byte code chunks in flight per lane per gather pass
 #endif
-#ifndef AQR_LPR_DIV
-#define AQR_LPR_DIV 1  // 2: each lane loads 32 B of a code row (half the lanes per row)
-#endif
 #ifndef AQR_PREFETCH_ROW
 #define AQR_PREFETCH_ROW 1
 #endif
@@ -118,15 +115,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-constexpr int kLinRegs = 12;  // C of up to 32 x 12 entries is linearized through registers
+// number of W keys strictly less than key, ignoring the expanded flag bit
+__device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if ((a[mid] & ~1ull) < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
 
 // ------------------------------------------------------------------------------------
 // per-warp shared-memory layout
 // ------------------------------------------------------------------------------------
 struct Layout {
   int o_qc, o_qf, o_w, o_h, o_s23, o_nb, o_nd, o_cand, o_cs, o_lb, o_bar, per_warp;
-  int region;     // bytes of the hash / block-buffer region
-  int wcap;       // W ring capacity (slots)
+  int region;     // bytes of the hash / block-buffer region (reused by Stage 2/3)
   int buf_bytes;  // INLINE: one staged block (128-byte aligned)
 };
 
@@ -137,13 +142,12 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c) {
   int o = 0;
   L.o_qc = o; o += al16(ix.d_pad);
   L.o_qf = o; o += al16(4 * ix.d4);
-  L.wcap = c.ef + ix.ld0;  // W ring slots (see the beam): ef + one layer-0 row of headroom
-  L.o_w = o; o += al16(8 * L.wcap);
+  L.o_w = o; o += al16(8 * (c.ef + 1));
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
   L.region = ix.blk ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
   o = (o + 127) & ~127;
   L.o_h = o; o += al16(L.region);
-  L.o_s23 = o; o += (c.n_coarse > 32 * kLinRegs || L.wcap < 2 * c.n_coarse) ? al16(8 * c.n_coarse) : 0;
+  L.o_s23 = o; o += c.ef >= 2 * c.n_coarse ? 0 : al16(8 * c.n_coarse);
   L.o_nb = o; o += al16(4 * ix.ld0);
   L.o_nd = o; o += al16(4 * ix.ld0);
   L.o_cand = o; o += al16(8 * ix.ld0);
@@ -626,35 +630,25 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
 #pragma unroll
       for (int t = 0; t < kRowRegs; ++t) {
         const int j = lane + 32 * t;
-        arow[t] = -1;
-        if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = __ldg(ix.adj0 + (int64_t)cur * ix.ld0 + j);
+        arow[t] = j < ix.cap0 ? __ldg(ix.adj0 + (int64_t)cur * ix.ld0 + j) : -1;
       }
     }
-    // W is a ring of wcap slots holding the sorted list in DESCENDING order: logical (ascending)
-    // index i lives in slot (tail - 1 - i) mod wcap.  New candidates land near the logical front
-    // (they are close to the query), so only the few entries in front of the last insertion point
-    // move; the entries behind it keep their slots (tail advances by np) and evicting the largest
-    // entries is free (they simply fall out of the logical range [0, ef)).
-    const int wcap = L.wcap;
-    int tail = 1;
-    auto slot = [&](int i, int t) { const int p = t - 1 - i; return p < 0 ? p + wcap : p; };
     int size = 1, cursor = 0, nexp = 0;
     for (;;) {
       // smallest unexpanded entry of W
       int pos = -1;
       for (int bb = cursor; bb < size; bb += 32) {
         const int i = bb + lane;
-        const bool un = i < size && !(W[slot(i, tail)] & 1ull);
+        const bool un = i < size && !(W[i] & 1ull);
         const uint32_t mk = __ballot_sync(kFull, un);
         if (mk) { pos = bb + __ffs(mk) - 1; break; }
       }
       if (pos < 0) break;
-      const int pslot = slot(pos, tail);
-      const uint64_t wk = W[pslot];
+      const uint64_t wk = W[pos];
       const int32_t cnode = qkey_id(wk);
       __syncwarp();
       if (lane == 0) {
-        W[pslot] = wk | 1ull;
+        W[pos] = wk | 1ull;
         if (has_dbg && dbg.exp_ids && nexp < dbg.exp_cap) dbg.exp_ids[qi * dbg.exp_cap + nexp] = cnode;
       }
       ++nexp;
@@ -683,15 +677,13 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
 #pragma unroll
           for (int t = 0; t < kRowRegs; ++t) {
             const int j = lane + 32 * t;
-            arow[t] = -1;
-            if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = __ldg(ix.adj0 + (int64_t)cnode * ix.ld0 + j);
+            arow[t] = j < ix.cap0 ? __ldg(ix.adj0 + (int64_t)cnode * ix.ld0 + j) : -1;
           }
         }
         int deg = 0;
         m = 0;
 #pragma unroll
         for (int t = 0; t < kRowRegs; ++t) {
-          if (32 * t >= ix.cap0) break;  // uniform
           const int32_t u = arow[t];
           deg += __popc(__ballot_sync(kFull, u >= 0));
           bool keep = u >= 0;
@@ -710,7 +702,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       // filter against max W (when full), then drop re-evaluations already in W (R15): the
       // survivors of the cheap key test are compacted first so the W binary search (which also
       // yields each candidate's insertion rank) runs once per survivor, not once per neighbour
-      const uint64_t maxk = size >= ef ? (W[slot(size - 1, tail)] & ~1ull) : ~0ull;
+      const uint64_t maxk = size >= ef ? (W[size - 1] & ~1ull) : ~0ull;
       int np0 = 0;
       for (int r0 = 0; r0 < m; r0 += 32) {
         const int r = r0 + lane;
@@ -735,16 +727,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         int lb = 0;
         if (j < np0) {
           kk = cs[j];
-          {  // lower bound of kk in logical [0, size)
-            int a = 0, z = size;
-            while (a < z) {
-              const int mid = (a + z) >> 1;
-              if ((W[slot(mid, tail)] & ~1ull) < kk) a = mid + 1;
-              else z = mid;
-            }
-            lb = a;
-          }
-          ok = !(lb < size && (W[slot(lb, tail)] & ~1ull) == kk);
+          lb = lower_bound_w(W, size, kk);
+          ok = !(lb < size && (W[lb] & ~1ull) == kk);
         }
         const uint32_t mk = __ballot_sync(kFull, ok);
         if (ok) {
@@ -763,10 +747,10 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         uint64_t kw = ~0ull;
         for (int bb = pos + 1; bb < size; bb += 32) {
           const int i = bb + lane;
-          const bool un = i < size && !(W[slot(i, tail)] & 1ull);
+          const bool un = i < size && !(W[i] & 1ull);
           const uint32_t mk = __ballot_sync(kFull, un);
           if (mk) {
-            kw = W[slot(bb + __ffs(mk) - 1, tail)];
+            kw = W[bb + __ffs(mk) - 1];
             break;
           }
         }
@@ -782,8 +766,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
 #pragma unroll
           for (int t = 0; t < kRowRegs; ++t) {
             const int j = lane + 32 * t;
-            arow[t] = -1;
-            if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = __ldg(ix.adj0 + rb + j);
+            arow[t] = j < ix.cap0 ? __ldg(ix.adj0 + rb + j) : -1;
           }
         }
       }
@@ -804,51 +787,27 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       }
       __syncwarp();
       const int first_ins = slb[0];
-      // Old entry i moves to logical i + sh(i), sh(i) = #{r : slb[r] <= i}.  The ring lets either
-      // end stay in place (a deque): keep the front fixed (tail unchanged) and move the entries at
-      // or behind the first insertion point (size - first_ins entries), or keep the back fixed
-      // (tail += np) and move the entries in front of the last insertion point (slb[np-1]
-      // entries) -- whichever moves fewer.  Entries whose new position is >= ef are evicted.
-      const int last = slb[np - 1];
-      int ntail = tail;
-      if (size - first_ins <= last) {
-        // front fixed: moves go to LOWER slots, so walk from the logical top down
-        int r_hi = np;
-        for (int hi = size; hi > first_ins; hi -= 32) {
-          const int lo = hi - 32 > first_ins ? hi - 32 : first_ins;
-          while (r_hi > 0 && slb[r_hi - 1] > hi - 1) --r_hi;
-          const int i = lo + lane;
-          int sh = r_hi;
-          for (int r = r_hi; r > 0 && slb[r - 1] > lo; --r) sh -= slb[r - 1] > i;
-          uint64_t v = 0;
-          if (i < hi) v = W[slot(i, tail)];
-          __syncwarp();
-          if (i < hi && i + sh < ef) W[slot(i + sh, tail)] = v;
-          __syncwarp();
-        }
-      } else {
-        // back fixed: moves go to HIGHER slots, so walk from logical 0 up
-        ntail = tail + np;
-        if (ntail >= wcap) ntail -= wcap;
-        int r_lo = 0;
-        for (int i0 = 0; i0 < last; i0 += 32) {
-          const int i1 = i0 + 32 < last ? i0 + 32 : last;
-          while (r_lo < np && slb[r_lo] <= i0) ++r_lo;
-          const int i = i0 + lane;
-          int sh = r_lo;
-          for (int r = r_lo; r < np && slb[r] <= i1 - 1; ++r) sh += slb[r] <= i;
-          uint64_t v = 0;
-          if (i < i1) v = W[slot(i, tail)];
-          __syncwarp();
-          if (i < i1 && i + sh < ef) W[slot(i + sh, ntail)] = v;
-          __syncwarp();
-        }
+      // shift the old entries W[first_ins:size) right, top chunk first (in place).  Entry i moves
+      // by sh(i) = #{r : slb[r] <= i}; walking down, r_hi tracks #{r : slb[r] <= hi - 1} and only
+      // the few candidates whose slb falls inside the chunk adjust individual lanes, so the whole
+      // shift costs O(chunks + np) uniform steps instead of a search per entry
+      int r_hi = np;
+      for (int hi = size; hi > first_ins; hi -= 32) {
+        const int lo = hi - 32 > first_ins ? hi - 32 : first_ins;
+        while (r_hi > 0 && slb[r_hi - 1] > hi - 1) --r_hi;
+        const int i = lo + lane;
+        int sh = r_hi;
+        for (int r = r_hi; r > 0 && slb[r - 1] > lo; --r) sh -= slb[r - 1] > i;
+        uint64_t v = 0;
+        if (i < hi) v = W[i];
+        __syncwarp();
+        if (i < hi && i + sh < ef) W[i + sh] = v;
+        __syncwarp();
       }
       for (int i = lane; i < np; i += 32) {
         const int dst = slb[i] + i;
-        if (dst < ef) W[slot(dst, ntail)] = cs[i];
+        if (dst < ef) W[dst] = cs[i];
       }
-      tail = ntail;
       __syncwarp();
       size = size + np < ef ? size + np : ef;
       cursor = first_ins < pos + 1 ? first_ins : pos + 1;
@@ -856,44 +815,23 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     cnt[0] = nexp;
     cnt[10] = fails;
 
-    // C = the first nc logical entries of W, linearized (ascending) for Stage 2/3: through
-    // registers into W[0:nc) when it fits (the rest of the ring is free scratch), else copied
-    // to the separate s23 area
+    // debug: C with d^q
     const int nc = c.n_coarse < size ? c.n_coarse : size;
-    __syncwarp();
-    uint64_t* lin;
-    uint64_t* akeys;
-    if (nc <= 32 * kLinRegs) {
-      uint64_t tmp[kLinRegs];
-#pragma unroll
-      for (int j = 0; j < kLinRegs; ++j) {
-        const int i = lane + 32 * j;
-        tmp[j] = i < nc ? W[slot(i, tail)] : 0ull;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < kLinRegs; ++j) {
-        const int i = lane + 32 * j;
-        if (i < nc) W[i] = tmp[j];
-      }
-      lin = W;
-      akeys = wcap >= 2 * nc ? W + nc : reinterpret_cast<uint64_t*>(wb + L.o_s23);
-    } else {
-      lin = reinterpret_cast<uint64_t*>(wb + L.o_s23);
-      for (int i = lane; i < nc; i += 32) lin[i] = W[slot(i, tail)];
-      akeys = W;
-    }
     __syncwarp();
     if (has_dbg) {
       for (int i = lane; i < c.n_coarse; i += 32) {
-        const uint64_t wkk = i < nc ? lin[i] : 0;
+        const uint64_t wkk = i < nc ? W[i] : 0;
         if (dbg.coarse_ids) dbg.coarse_ids[qi * c.n_coarse + i] = i < nc ? qkey_id(wkk) : -1;
         if (dbg.coarse_dq) dbg.coarse_dq[qi * c.n_coarse + i] = i < nc ? (int32_t)qkey_d(wkk) : -1;
       }
     }
+    // Stage 2/3 scratch lives in W: unsorted keys overwrite W[0:nc] in place, A goes to
+    // W[nc:2nc] (ef >= 2 N_c, as with m_ef >= 2), else to a separate area
+    uint64_t* akeys = ef >= 2 * nc ? W + nc : reinterpret_cast<uint64_t*>(wb + L.o_s23);
+    uint64_t* rkeys = W;
     __syncwarp();
-    // 4-7. Stage 2, early termination, Stage 3, assembly (unsorted keys overwrite lin in place)
-    finish_query(ix, c, qf, nullptr, lin, nc, akeys, lin, qi, out_ids, out_dist, dbg, has_dbg != 0, lane, cnt);
+    // 4-7. Stage 2, early termination, Stage 3, assembly
+    finish_query(ix, c, qf, nullptr, W, nc, akeys, rkeys, qi, out_ids, out_dist, dbg, has_dbg != 0, lane, cnt);
     if (has_dbg && lane == 0) {
       if (dbg.counters)
         for (int t = 0; t < AQR_NCOUNT; ++t) dbg.counters[qi * AQR_NCOUNT + t] = cnt[t];
@@ -988,20 +926,14 @@ size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int wpb) {
 cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                           int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
                           cudaStream_t s) {
-  // lanes per code row: the next power of two >= the row's 16-byte chunks, divided by
-  // AQR_LPR_DIV (each lane then loads CPL chunks of the row), capped at 32
   const int nch = ix.d_pad >> 4;
-  int p2 = 1;
-  while (p2 < nch) p2 <<= 1;
-  int lpr = p2 / AQR_LPR_DIV;
-  if (lpr < 1) lpr = 1;
-  if (lpr > 32) lpr = 32;
+  int lpr = 1;
+  while (lpr < nch && lpr < 32) lpr <<= 1;
   const int cpl = (nch + lpr - 1) / lpr;
   const bool inl = ix.blk != nullptr;
 #define AQR_LAUNCH(L_, C_)                                                                               \
   return inl ? launch_t<L_, C_, true>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)      \
              : launch_t<L_, C_, false>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)
-#if AQR_LPR_DIV == 1
   switch (lpr) {
     case 1: AQR_LAUNCH(1, 1);
     case 2: AQR_LAUNCH(2, 1);
@@ -1014,19 +946,6 @@ cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* 
       if (cpl <= 4) AQR_LAUNCH(32, 4);
       return cudaErrorInvalidValue;
   }
-#else
-  switch (lpr) {
-    case 1: if (cpl == 1) AQR_LAUNCH(1, 1); AQR_LAUNCH(1, 2);
-    case 2: AQR_LAUNCH(2, 2);
-    case 4: AQR_LAUNCH(4, 2);
-    case 8: AQR_LAUNCH(8, 2);
-    case 16: AQR_LAUNCH(16, 2);
-    default:
-      if (cpl <= 2) AQR_LAUNCH(32, 2);
-      if (cpl <= 4) AQR_LAUNCH(32, 4);
-      return cudaErrorInvalidValue;
-  }
-#endif
 #undef AQR_LAUNCH
 }
 
