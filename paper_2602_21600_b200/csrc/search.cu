@@ -38,6 +38,9 @@ namespace {
 #ifndef AQR_ROWS_PER_PASS
 #define AQR_ROWS_PER_PASS 16  // 16-byte code chunks in flight per lane per gather pass
 #endif
+#ifndef AQR_LPR_DIV
+#define AQR_LPR_DIV 1  // 2: each lane loads 32 B of a code row (half the lanes per row)
+#endif
 #ifndef AQR_PREFETCH_ROW
 #define AQR_PREFETCH_ROW 1
 #endif
@@ -630,7 +633,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
 #pragma unroll
       for (int t = 0; t < kRowRegs; ++t) {
         const int j = lane + 32 * t;
-        arow[t] = j < ix.cap0 ? __ldg(ix.adj0 + (int64_t)cur * ix.ld0 + j) : -1;
+        arow[t] = -1;
+        if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = __ldg(ix.adj0 + (int64_t)cur * ix.ld0 + j);
       }
     }
     int size = 1, cursor = 0, nexp = 0;
@@ -677,13 +681,15 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
 #pragma unroll
           for (int t = 0; t < kRowRegs; ++t) {
             const int j = lane + 32 * t;
-            arow[t] = j < ix.cap0 ? __ldg(ix.adj0 + (int64_t)cnode * ix.ld0 + j) : -1;
+            arow[t] = -1;
+            if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = __ldg(ix.adj0 + (int64_t)cnode * ix.ld0 + j);
           }
         }
         int deg = 0;
         m = 0;
 #pragma unroll
         for (int t = 0; t < kRowRegs; ++t) {
+          if (32 * t >= ix.cap0) break;  // uniform
           const int32_t u = arow[t];
           deg += __popc(__ballot_sync(kFull, u >= 0));
           bool keep = u >= 0;
@@ -766,7 +772,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
 #pragma unroll
           for (int t = 0; t < kRowRegs; ++t) {
             const int j = lane + 32 * t;
-            arow[t] = j < ix.cap0 ? __ldg(ix.adj0 + rb + j) : -1;
+            arow[t] = -1;
+            if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = __ldg(ix.adj0 + rb + j);
           }
         }
       }
@@ -926,14 +933,20 @@ size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int wpb) {
 cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                           int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
                           cudaStream_t s) {
+  // lanes per code row: the next power of two >= the row's 16-byte chunks, divided by
+  // AQR_LPR_DIV (each lane then loads CPL chunks of the row), capped at 32
   const int nch = ix.d_pad >> 4;
-  int lpr = 1;
-  while (lpr < nch && lpr < 32) lpr <<= 1;
+  int p2 = 1;
+  while (p2 < nch) p2 <<= 1;
+  int lpr = p2 / AQR_LPR_DIV;
+  if (lpr < 1) lpr = 1;
+  if (lpr > 32) lpr = 32;
   const int cpl = (nch + lpr - 1) / lpr;
   const bool inl = ix.blk != nullptr;
 #define AQR_LAUNCH(L_, C_)                                                                               \
   return inl ? launch_t<L_, C_, true>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)      \
              : launch_t<L_, C_, false>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)
+#if AQR_LPR_DIV == 1
   switch (lpr) {
     case 1: AQR_LAUNCH(1, 1);
     case 2: AQR_LAUNCH(2, 1);
@@ -946,6 +959,19 @@ cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* 
       if (cpl <= 4) AQR_LAUNCH(32, 4);
       return cudaErrorInvalidValue;
   }
+#else
+  switch (lpr) {
+    case 1: if (cpl == 1) AQR_LAUNCH(1, 1); AQR_LAUNCH(1, 2);
+    case 2: AQR_LAUNCH(2, 2);
+    case 4: AQR_LAUNCH(4, 2);
+    case 8: AQR_LAUNCH(8, 2);
+    case 16: AQR_LAUNCH(16, 2);
+    default:
+      if (cpl <= 2) AQR_LAUNCH(32, 2);
+      if (cpl <= 4) AQR_LAUNCH(32, 4);
+      return cudaErrorInvalidValue;
+  }
+#endif
 #undef AQR_LAUNCH
 }
 
