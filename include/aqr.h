@@ -118,7 +118,7 @@ typedef struct {
  *          those neighbours (n x 2M x d_pad bytes, ~7 GB for 1M x 128 at M = 27); an expansion
  *          is ONE bulk (TMA) copy of that block into shared memory, prefetched while the
  *          previous expansion's merge runs.  Uses HBM capacity to remove a round trip.
- *  AUTO:   INLINE when the blocks fit in 40% of the free device memory, else GATHER.
+ *  AUTO:   GATHER (measured faster on B200 at every C2 ef point, profiles/r01).
  * Both layouts give identical results (same visit order, same ids). */
 enum { AQR_LAYOUT_AUTO = 0, AQR_LAYOUT_GATHER = 1, AQR_LAYOUT_INLINE = 2 };
 

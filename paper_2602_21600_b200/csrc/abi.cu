@@ -206,13 +206,10 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   V.blk_ids = round_up(4 * cap0, 16);
   V.blk_bytes = V.blk_ids + cap0 * D.d_pad;
   V.blk_stride = (V.blk_bytes + 127) / 128 * 128;
-  // layer-0 layout (include/aqr.h): INLINE blocks when they fit
+  // layer-0 layout (include/aqr.h): AUTO = GATHER (measured faster on B200: the INLINE block
+  // buffer costs occupancy and moves every neighbour row, profiles/r01)
   const size_t blk_total = (size_t)n * (size_t)V.blk_stride;
-  bool inl = D.layout == AQR_LAYOUT_INLINE;
-  if (D.layout == AQR_LAYOUT_AUTO) {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) inl = blk_total <= (size_t)(0.4 * (double)free_b);
-  }
+  const bool inl = D.layout == AQR_LAYOUT_INLINE;
   if (inl) {
     uint8_t* blk = (uint8_t*)alloc(blk_total);
     if (!blk) {

@@ -1,0 +1,96 @@
+"""Multi-GPU plumbing of the batched search: one process per GPU, torch.distributed.
+
+* C1-C4 -- replicas.  Every rank holds the whole index; the query batch is split contiguously
+  (`query_range`) or, for weak scaling, every rank searches its own full batch.  No collective
+  on the data path; `gather_rows` collects per-rank result rows for reporting only.
+* C5 -- the base is sharded S ways (BASELINE.json configs[4]); rank r holds the shards
+  `shards_of_rank(S, world, r)`, each a complete AQR index whose ids are offset by the shard's
+  first row (`shard_rows`, passed to aqr_upload_index as id_base).  Per rank the per-shard top-k
+  lists are merged by aqr_merge_topk, the per-rank lists are gathered over NCCL
+  (`all_gather_into_tensor` of [nq x k] dists + ids, NVLink / NVSwitch) and merged again
+  (`gather_merge`).  The merge orders by (dist, global id), so the output is
+  identical for every world size.
+
+Only plumbing lives here: the merge itself is a callable (aqr.merge_topk on the GPU path; the
+CPU tests pass the oracle's merge through gloo).
+"""
+from __future__ import annotations
+
+
+def query_range(nq: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous query slice [lo, hi) of `rank` (sizes differ by at most one)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    return rank * nq // world, (rank + 1) * nq // world
+
+
+def shard_rows(n_total: int, n_shards: int, s: int) -> tuple[int, int]:
+    """Base rows [lo, hi) of shard s (C5: 8 shards of 1.25M rows; shard base = lo = id_base)."""
+    if n_shards < 1 or not 0 <= s < n_shards:
+        raise ValueError("bad shard")
+    return s * n_total // n_shards, (s + 1) * n_total // n_shards
+
+
+def shards_of_rank(n_shards: int, world: int, rank: int) -> list[int]:
+    """Shards held by `rank`: a contiguous block of n_shards / world (world must divide n_shards
+    or exceed it; with world > n_shards the extra ranks hold nothing)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    if world <= n_shards:
+        if n_shards % world:
+            raise ValueError("world size must divide the shard count")
+        per = n_shards // world
+        return list(range(rank * per, (rank + 1) * per))
+    return [rank] if rank < n_shards else []
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def all_gather_lists(dist_t, ids_t, group=None):
+    """[nq, k] dists (fp32) + ids (int32) of every rank -> [world, nq, k] each, rank order."""
+    import torch
+    d = _dist()
+    world = d.get_world_size(group)
+    if world == 1:
+        return dist_t.unsqueeze(0), ids_t.unsqueeze(0)
+    nq, k = dist_t.shape
+    od = torch.empty((world, nq, k), dtype=dist_t.dtype, device=dist_t.device)
+    oi = torch.empty((world, nq, k), dtype=ids_t.dtype, device=ids_t.device)
+    if d.get_backend(group) == "nccl":
+        d.all_gather_into_tensor(od, dist_t.contiguous(), group=group)
+        d.all_gather_into_tensor(oi, ids_t.contiguous(), group=group)
+    else:  # gloo (CPU tests): list form
+        d.all_gather(list(od.unbind(0)), dist_t.contiguous(), group=group)
+        d.all_gather(list(oi.unbind(0)), ids_t.contiguous(), group=group)
+    return od, oi
+
+
+def gather_merge(dist_t, ids_t, merge_fn, group=None):
+    """Merge this rank's [nq, k] top-k list with every other rank's: all-gather, then
+    merge_fn([world, nq, k] dists, ids) -> ([nq, k], [nq, k]) on every rank."""
+    od, oi = all_gather_lists(dist_t, ids_t, group)
+    if od.shape[0] == 1:
+        return dist_t, ids_t
+    return merge_fn(od, oi)
+
+
+def gather_rows(t, group=None):
+    """Concatenate per-rank row blocks (possibly of different lengths) in rank order."""
+    import torch
+    d = _dist()
+    world = d.get_world_size(group)
+    if world == 1:
+        return t
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    d.all_gather(ns, n, group=group)
+    ns = [int(v.item()) for v in ns]
+    mx = max(ns)
+    pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[: t.shape[0]] = t
+    outs = [torch.empty_like(pad) for _ in range(world)]
+    d.all_gather(outs, pad, group=group)
+    return torch.cat([o[:m] for o, m in zip(outs, ns)])

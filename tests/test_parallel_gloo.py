@@ -1,0 +1,91 @@
+"""N > 1 host path on CPU: world_size-2 gloo process groups.
+
+The sharded (C5) path gathers every rank's per-shard-merged top-k lists and merges them again;
+the result must be byte-identical to one merge over all shards (the merge orders by
+(dist, global id), BASELINE.json configs[4]).  The merge used here is the oracle's
+(oracle.merge_topk); on the GPU the same plumbing calls aqr.merge_topk."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2602_21600_b200 import parallel as P
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _shard_lists(S, nq, k, seed=5):
+    """Per-shard sorted (dist, global id) lists with many exact distance ties and short lists."""
+    rng = np.random.default_rng(seed)
+    d = rng.integers(0, 30, size=(S, nq, k)).astype(np.float32) / 8
+    ids = np.stack([rng.permutation(5000)[: nq * k].reshape(nq, k) + s * 5000 for s in range(S)]).astype(np.int32)
+    order = np.lexsort((ids, d), axis=-1)
+    d = np.take_along_axis(d, order, -1)
+    ids = np.take_along_axis(ids, order, -1)
+    d[1, 3, -4:] = np.inf  # a short shard list (padded with (-1, +inf))
+    ids[1, 3, -4:] = -1
+    return d, ids
+
+
+def _merge(od, oi):
+    k = od.shape[-1]
+    md, mi = oracle.merge_topk(od.numpy(), oi.numpy(), k)
+    return torch.from_numpy(md), torch.from_numpy(mi)
+
+
+def _worker(rank, world, port, S, nq, k, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        d, ids = _shard_lists(S, nq, k)
+        mine = P.shards_of_rank(S, world, rank)
+        # local merge over this rank's shards, then the cross-rank gather + merge
+        ld, li = _merge(torch.from_numpy(d[mine]), torch.from_numpy(ids[mine]))
+        gd, gi = P.gather_merge(ld, li, _merge)
+        # replicated path: each rank's query slice, gathered back in rank order
+        lo, hi = P.query_range(nq, world, rank)
+        rows = P.gather_rows(torch.arange(lo, hi, dtype=torch.int64))
+        np.save(os.path.join(out_dir, f"r{rank}_d.npy"), gd.numpy())
+        np.save(os.path.join(out_dir, f"r{rank}_i.npy"), gi.numpy())
+        np.save(os.path.join(out_dir, f"r{rank}_rows.npy"), rows.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_gather_merge_gloo(tmp_path, world):
+    S, nq, k = 8, 37, 12
+    mp.spawn(_worker, args=(world, _free_port(), S, nq, k, str(tmp_path)), nprocs=world, join=True)
+    d, ids = _shard_lists(S, nq, k)
+    ref_d, ref_i = oracle.merge_topk(d, ids, k)
+    for r in range(world):
+        np.testing.assert_array_equal(np.load(tmp_path / f"r{r}_i.npy"), ref_i)
+        np.testing.assert_array_equal(np.load(tmp_path / f"r{r}_d.npy").view(np.uint32), ref_d.view(np.uint32))
+        np.testing.assert_array_equal(np.load(tmp_path / f"r{r}_rows.npy"), np.arange(nq))
+
+
+def test_partitions():
+    for nq in [0, 1, 7, 10_000]:
+        for world in [1, 2, 3, 8]:
+            spans = [P.query_range(nq, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == nq
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+    for world in [1, 2, 4, 8]:
+        got = sorted(s for r in range(world) for s in P.shards_of_rank(8, world, r))
+        assert got == list(range(8))
+    assert [P.shard_rows(10_000_000, 8, s) for s in (0, 7)] == [(0, 1_250_000), (8_750_000, 10_000_000)]
+    with pytest.raises(ValueError):
+        P.shards_of_rank(8, 3, 0)
