@@ -209,7 +209,7 @@ def bytes_per_query(tot, nq, d, k, distinct_ratio=1.0):
     counts every neighbour it scores (it keeps no exact visited set); `distinct_ratio` = distinct
     evaluations / neighbours scored, measured exactly by the oracle (same visit order) on a query
     sample, converts that count to the algorithmic one."""
-    exp, deg, ev, uexp, udeg, uev, nc, depth, et, na, fails = [float(v) for v in tot]
+    exp, deg, ev, uexp, udeg, uev, nc, depth, et, na, fails = [float(v) for v in tot[:11]]
     b = (4 * d * nq + 4 * (deg + exp) + 4 * (udeg + uexp) + d * ((ev - fails) * distinct_ratio + uev) + d * nc
          + 4 * d * depth + 8 * k * nq)
     return b / nq
@@ -481,6 +481,156 @@ def cpu_baseline(w, oix, m, k, seconds, searcher):
 
 
 # --------------------------------------------------------------------------------------------
+# C5: the base sharded 8 ways; per-shard top-k merged locally, then over NCCL
+# --------------------------------------------------------------------------------------------
+def run_sharded(args):
+    import torch
+    import synth
+    import paper_2602_21600_b200 as aqr
+    from paper_2602_21600_b200 import evaluate as E
+    from paper_2602_21600_b200 import graph as G
+    from paper_2602_21600_b200 import parallel as P
+
+    rank, world, local = dist_init(args.gpus)
+    S = 8
+    n_shard = max(1, int(round(1_250_000 * args.scale)))
+    nq = args.nq or 10_000
+    k = 100
+    ef = 128 if args.ef == "auto" else int(args.ef)
+    m = aqr.ef_mapping(ef, k)
+    q_host = synth.gen_c5_queries(nq)  # every rank generates the same queries from the seed
+    q = torch.from_numpy(q_host).cuda()
+    mine = P.shards_of_rank(S, world, rank)
+    threads = args.threads or max(1, (os.cpu_count() or 1) // min(world, 8))
+    shards, infos = [], []
+    gt_d_parts, gt_i_parts = [], []
+    for s_ in mine:
+        t0 = time.time()
+        xs = synth.gen_c5_shard(s_, n_shard)
+        x = torch.from_numpy(xs).cuda()
+        samp = synth.density_sample(n_shard, cfg="C5")
+        codes, quant = aqr.encode(x, sample_idx=torch.from_numpy(samp).cuda(), p_max=P_MAX["C5"], want_rho=True)
+        torch.cuda.synchronize()
+        eta = G.eta_of(G.density_weights(xs[samp], quant.rho.cpu().numpy()))
+        M, efc = G.adapt_params(32, 200, quant.delta, eta)
+        g = G.build_hnsw(codes.cpu().numpy(), M, efc, synth.level_draws(n_shard, cfg="C5", shard=s_), threads,
+                         flags=BUILD_FLAGS)
+        ix = aqr.upload_index(codes, x, quant, g, metric="l2", id_base=s_ * n_shard, layout=LAYOUT)
+        shards.append((x, ix, aqr.Searcher(ix, nq, aqr.make_params(k, **m))))
+        # exact ground truth of this shard (global ids), merged across shards below
+        gi, gd = E.ground_truth(x, q, k)
+        gt_i_parts.append(gi + s_ * n_shard)
+        gt_d_parts.append(gd)
+        infos.append(dict(shard=s_, M=M, efc=efc, delta=quant.delta, eta=eta, max_level=g.max_level,
+                          build_s=round(time.time() - t0, 1), index_bytes=ix.device_bytes()))
+        if rank == 0:
+            log(f"[bench] C5 shard {s_}: {infos[-1]}")
+
+    def step():
+        outs = [sh[2].run(q) for sh in shards]
+        if len(outs) == 1:
+            ld, li = outs[0][1], outs[0][0]
+        else:
+            ld, li = aqr.merge_topk(torch.stack([o[1] for o in outs]), torch.stack([o[0] for o in outs]))
+        return P.gather_merge(ld, li, aqr.merge_topk)
+
+    # recall@10 / @100 against the merged exact ground truth (C5 is continuous: no exact ties)
+    fd, fi = step()
+    torch.cuda.synchronize()
+    gd_all = np.concatenate(gt_d_parts, 1)
+    gi_all = np.concatenate(gt_i_parts, 1)
+    if world > 1:
+        td, ti = P.all_gather_lists(torch.from_numpy(gd_all).cuda(), torch.from_numpy(gi_all).cuda())
+        gd_all = np.concatenate(list(td.cpu().numpy()), 1)
+        gi_all = np.concatenate(list(ti.cpu().numpy()), 1)
+    order = np.lexsort((gi_all, gd_all), axis=1)[:, :k]
+    gt_ids = np.take_along_axis(gi_all, order, 1)
+    found = fi.cpu().numpy()
+    r10 = E.recall(found, gt_ids, k=10)[0]
+    r100 = E.recall(found, gt_ids, k=100)[0]
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = Clocks(local)
+    clocks.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    ms = allreduce_max(e0.elapsed_time(e1) / args.steps, world)
+    value = nq / (ms / 1e3)
+    # search-kernel share + counters (one untimed stats pass)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for sh in shards:
+        sh[2].run(q)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kern_ms = k0.elapsed_time(k1)
+    bq_tot = 0.0
+    for sh in shards:
+        sh[2].totals.zero_()
+        sh[2].run(q, stats=True)
+        torch.cuda.synchronize()
+        bq_tot += bytes_per_query(sh[2].totals.cpu().numpy(), nq, 96, k, 1.0)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bq_tot * nq / (kern_ms / 1e3) / 1e9
+    # end to end: pinned host queries in, host top-k out
+    qh = torch.from_numpy(q_host).pin_memory()
+    ids_h = torch.empty((nq, k), dtype=torch.int32).pin_memory()
+    dist_h = torch.empty((nq, k), dtype=torch.float32).pin_memory()
+    barrier(world)
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(args.steps):
+        q.copy_(qh, non_blocking=True)  # step() searches q
+        rd, ri = step()
+        ids_h.copy_(ri, non_blocking=True)
+        dist_h.copy_(rd, non_blocking=True)
+    a1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = allreduce_max(a0.elapsed_time(a1) / args.steps, world)
+    if rank == 0:
+        line = {
+            "metric": "QPS (C5 sharded, recall@10 reported)", "value": round(value, 1), "unit": "queries/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8+int32+f32",
+            "data": "synthetic (seeded, BASELINE.json configs[4] recipe)",
+            "config": {"workload": f"C5: {S} shards x {n_shard} x 96 l2, {nq} queries, k={k}", "ef": m["ef"],
+                       "n_coarse": m["n_coarse"], "n_rerank": m["n_rerank"], "recall@10": round(r10, 4),
+                       "recall@100": round(r100, 4), "parallelism": f"{S} shards over {world} GPU(s), NCCL all-gather + merge",
+                       "shards_per_rank": len(mine), "l2": "shard indexes > 126 MB L2; no flush", "shards": infos},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None, "bytes_per_query": round(bq_tot, 1),
+                         "kernel": "search_kernel (all shards of rank 0)", "kernel_ms": round(kern_ms, 4),
+                         "note": "bytes from kernel counters, re-evaluations counted (distinct ratio 1)"},
+            "cpu_baseline": None,
+            "e2e": {"value": round(nq / (e2e_ms / 1e3), 1), "unit": "queries/s", "h2d_bytes_per_step": int(q_host.nbytes),
+                    "d2h_bytes_per_step": int(nq * k * 8)},
+            "gpu_launches": args.steps * (len(shards) + (1 if len(shards) > 1 else 0) + (1 if world > 1 else 0)),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------------------------
 # the reference arm: the CPU oracle as it stands (this tier has no reference implementation)
 # --------------------------------------------------------------------------------------------
 def run_reference(args):
@@ -564,6 +714,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "C5":
+        run_sharded(args)
     else:
         run_aqr(args)
 

@@ -154,10 +154,13 @@ typedef struct {
   int32_t warps_per_block; /* reserved, must be 0 (the CTA shape is fixed at compile time) */
 } aqr_search_params;
 
-#define AQR_NCOUNT 11
+#define AQR_NCOUNT 15
 /* counter slots: 0 expansions, 1 layer-0 degree sum, 2 layer-0 code evaluations, 3 upper
  * expansions, 4 upper degree sum, 5 upper evaluations, 6 |C|, 7 re-rank depth, 8 early-term
- * flag, 9 |A|, 10 visited-hash insert failures (re-evaluations allowed by DESIGN.md R15) */
+ * flag, 9 |A|, 10 visited-hash insert failures (re-evaluations allowed by DESIGN.md R15),
+ * 11 evaluations below the W threshold, 12 W insertions (11 minus re-evaluations already in
+ * W), 13 W buffer flushes, 14 expansions whose node was the smallest unexpanded W entry
+ * before the previous expansion's insert (kernel bookkeeping; no oracle counterpart) */
 
 /* Optional transcript (all device pointers, each may be NULL).  Per-query arrays are laid
  * out [nq x ...].  Used by the parity tests to compare visit order with the oracle. */

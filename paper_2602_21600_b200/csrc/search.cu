@@ -73,6 +73,10 @@ __device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
   uint32_t lo = __shfl_xor_sync(kFull, (uint32_t)v, m), hi = __shfl_xor_sync(kFull, (uint32_t)(v >> 32), m);
   return ((uint64_t)hi << 32) | lo;
 }
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+  uint32_t lo = __shfl_sync(kFull, (uint32_t)v, src), hi = __shfl_sync(kFull, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
 #pragma unroll
   for (int m = 16; m; m >>= 1) {
@@ -745,6 +749,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         }
         np += __popc(mk);
       }
+      cnt[11] += np0;
+      cnt[12] += np;
       {
         // the next expansion is min(first unexpanded entry of W after pos, smallest candidate);
         // start loading its layer-0 data now so the load overlaps the merge (prefetch only,
@@ -782,8 +788,48 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         cursor = pos + 1;
         continue;
       }
-      // merge: sorted candidate r lands at slb[r] + r (slb = #W keys below it, from the filter);
-      // an old entry W[i] moves right by #{r : slb[r] <= i}
+      // merge: candidate c lands at lb(c) + rank(c) (lb = #W keys below it, from the filter; rank =
+      // #candidates below it); an old entry W[p] moves right by #{c : lb(c) <= p}
+      if (np <= 32) {
+        // the usual case: candidates held one per lane; the shift amounts come from shuffles, so
+        // each group of 4 chunks is one batch of independent loads, then one batch of stores
+        const bool act = lane < np;
+        const uint64_t kk = act ? cand[lane] : ~0ull;
+        const int lbv = act ? clb[lane] : INT_MAX;
+        int rk = 0;
+        for (int j = 0; j < np; ++j) rk += shfl_u64(kk, j) < kk;
+        int first_ins = lbv;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) first_ins = min(first_ins, __shfl_xor_sync(kFull, first_ins, off));
+        for (int hi = size; hi > first_ins; hi -= 128) {
+          const int lo = hi - 128 > first_ins ? hi - 128 : first_ins;
+          uint64_t v[4];
+          int sh[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int p = lo + 32 * t + lane;
+            v[t] = p < hi ? W[p] : 0ull;
+            sh[t] = 0;
+          }
+          for (int j = 0; j < np; ++j) {
+            const int l = __shfl_sync(kFull, lbv, j);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) sh[t] += l <= lo + 32 * t + lane;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int p = lo + 32 * t + lane;
+            if (p < hi && p + sh[t] < ef) W[p + sh[t]] = v[t];
+          }
+          __syncwarp();
+        }
+        if (act && lbv + rk < ef) W[lbv + rk] = kk;
+        __syncwarp();
+        size = size + np < ef ? size + np : ef;
+        cursor = first_ins < pos + 1 ? first_ins : pos + 1;
+        continue;
+      }
       int32_t* slb = reinterpret_cast<int32_t*>(nd);
       for (int i = lane; i < np; i += 32) {
         const uint64_t kk = cand[i];

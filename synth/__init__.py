@@ -190,9 +190,14 @@ def density_sample(n: int, seed: int = 0, cfg: str = "C2", threshold: int = 10_0
     return np.sort(idx).astype(np.int32)
 
 
-def level_draws(n: int, seed: int = 0, cfg: str = "C2") -> np.ndarray:
-    """U in (0, 1] per node, in insertion (id) order, for the HNSW level assignment."""
-    return (1.0 - _rng(seed, cfg, 4).random(n)).astype(np.float64)
+def level_draws(n: int, seed: int = 0, cfg: str = "C2", shard: int | None = None) -> np.ndarray:
+    """U in (0, 1] per node, in insertion (id) order, for the HNSW level assignment (C5: one
+    independent stream per shard)."""
+    if shard is None:
+        r = _rng(seed, cfg, 4)
+    else:
+        r = np.random.default_rng(np.random.SeedSequence([int(seed), CFG_IDS.get(cfg, 99), 4, int(shard)]))
+    return (1.0 - r.random(n)).astype(np.float64)
 
 
 def sha256(a: np.ndarray) -> str:
