@@ -123,7 +123,7 @@ typedef struct {
 enum { AQR_LAYOUT_AUTO = 0, AQR_LAYOUT_GATHER = 1, AQR_LAYOUT_INLINE = 2 };
 
 /* Copy the index into library-owned device buffers re-laid-out for the search kernel
- * (code rows of d_pad bytes, fp32 rows padded to a multiple of 4 floats, layer-0 rows padded
+ * (code rows padded with zeros to a multiple of 32 bytes, one 256-bit load per 32 bytes, fp32 rows padded to a multiple of 4 floats, layer-0 rows padded
  * to a multiple of 8 entries).  The caller may free its inputs once the stream is
  * synchronized (this call synchronizes the stream before returning).  Validates ids,
  * entry point and sizes (AQR_E_INVALID). */

@@ -153,7 +153,7 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   aqr::IndexView& V = ix->v;
   V.n = n;
   V.d = D.d;
-  V.d_pad = D.d_pad;
+  V.d_pad = round_up(D.d, 32);  // internal code stride: whole 32-byte chunks (one LDG.256 each)
   V.d4 = round_up(D.d, 4);
   V.metric = (int32_t)D.metric;
   V.id_base = D.id_base;
@@ -162,7 +162,7 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   V.ld0 = round_up(cap0, 8);
   V.max_level = D.max_level;
   V.entry = D.entry_point;
-  uint8_t* codes = (uint8_t*)alloc((size_t)n * D.d_pad);
+  uint8_t* codes = (uint8_t*)alloc((size_t)n * V.d_pad);
   float* base = (float*)alloc(sizeof(float) * (size_t)n * V.d4);
   float* mn = (float*)alloc(sizeof(float) * V.d4);
   float* sc = (float*)alloc(sizeof(float) * V.d4);
@@ -175,7 +175,8 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   }
   cudaError_t e = cudaSuccess;
   auto chk = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
-  chk(cudaMemcpyAsync(codes, D.codes, (size_t)n * D.d_pad, cudaMemcpyDeviceToDevice, s));
+  if (V.d_pad != D.d_pad) chk(cudaMemsetAsync(codes, 0, (size_t)n * V.d_pad, s));
+  chk(cudaMemcpy2DAsync(codes, V.d_pad, D.codes, D.d_pad, D.d_pad, n, cudaMemcpyDeviceToDevice, s));
   if (V.d4 != D.d) chk(cudaMemsetAsync(base, 0, sizeof(float) * (size_t)n * V.d4, s));
   chk(cudaMemcpy2DAsync(base, sizeof(float) * V.d4, D.base, sizeof(float) * D.ld_base, sizeof(float) * D.d, n,
                         cudaMemcpyDeviceToDevice, s));
@@ -204,7 +205,7 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   V.up_off = uo;
   V.blk = nullptr;
   V.blk_ids = round_up(4 * cap0, 16);
-  V.blk_bytes = V.blk_ids + cap0 * D.d_pad;
+  V.blk_bytes = V.blk_ids + cap0 * V.d_pad;
   V.blk_stride = (V.blk_bytes + 127) / 128 * 128;
   // layer-0 layout (include/aqr.h): AUTO = GATHER (measured faster on B200: the INLINE block
   // buffer costs occupancy and moves every neighbour row, profiles/r01)

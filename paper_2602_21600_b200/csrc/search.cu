@@ -33,13 +33,10 @@ namespace {
 #define AQR_WARPS_PER_CTA 4
 #endif
 #ifndef AQR_MIN_CTAS
-#define AQR_MIN_CTAS 5  // 5 CTAs x 4 warps: the shared-memory limit at ef ~ 900 (<= 102 regs)
+#define AQR_MIN_CTAS 6  // 6 CTAs x 4 warps (<= 85 regs): the shared-memory limit at ef ~ 800
 #endif
 #ifndef AQR_ROWS_PER_PASS
 #define AQR_ROWS_PER_PASS 16  // 16-byte code chunks in flight per lane per gather pass
-#endif
-#ifndef AQR_LPR_DIV
-#define AQR_LPR_DIV 1  // 2: each lane loads 32 B of a code row (half the lanes per row)
 #endif
 #ifndef AQR_PREFETCH_ROW
 #define AQR_PREFETCH_ROW 1
@@ -84,15 +81,6 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
     v = o < v ? o : v;
   }
   return v;
-}
-
-// streaming 16-byte gather: read-only path, no L1 allocation (codes are touched once per query)
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
 }
 
 // ---- mbarrier + bulk (TMA) copy helpers (sm_90+ PTX; UBLKCP in SASS) ----
@@ -155,7 +143,19 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c) {
   o = (o + 127) & ~127;
   L.o_h = o; o += al16(L.region);
   L.o_s23 = o; o += c.ef >= 2 * c.n_coarse ? 0 : al16(8 * c.n_coarse);
-  L.o_nb = o; o += al16(4 * ix.ld0);
+  // nb is read in whole list_dists passes (G * U rows, the same LPR / CPL choice as
+  // launch_search), so it is padded to one
+  {
+    const int nch = ix.d_pad >> 5;
+    int lpr = 1;
+    while (lpr < nch) lpr <<= 1;
+    if (lpr > 32) lpr = 32;
+    const int cpl = (nch + lpr - 1) / lpr;
+    const int u = AQR_ROWS_PER_PASS / (2 * cpl) < 4 ? 4 : AQR_ROWS_PER_PASS / (2 * cpl) / 4 * 4;
+    const int pass = (32 / lpr) * u;
+    const int rows = (ix.ld0 + pass - 1) / pass * pass;
+    L.o_nb = o; o += al16(4 * (rows > ix.M ? rows : ix.M));
+  }
   L.o_nd = o; o += al16(4 * ix.ld0);
   L.o_cand = o; o += al16(8 * ix.ld0);
   L.o_cs = o; o += al16(8 * ix.ld0);
@@ -196,29 +196,88 @@ __device__ __forceinline__ void reduce_rows(int (&part)[U], int sub) {
 }
 
 // ------------------------------------------------------------------------------------
-// d^q for a list of node ids: LPR lanes per code row, CPL 16-byte chunks per lane
+// d^q for a list of node ids: LPR lanes per code row, CPL 32-byte chunks per lane (one
+// LDG.256 each; code rows are padded to a multiple of 32 bytes at upload)
 // d^q = sum q^2 + sum x^2 - 2 sum q x  (exact int32; dp4a on u8x4 words)
 // ------------------------------------------------------------------------------------
+struct C32 {
+  uint4 a, b;
+};
+
+__device__ __forceinline__ void ldg256(const void* p, C32& v) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.a.x), "=r"(v.a.y), "=r"(v.a.z), "=r"(v.a.w), "=r"(v.b.x), "=r"(v.b.y), "=r"(v.b.z),
+                 "=r"(v.b.w)
+               : "l"(p));
+}
+
+__device__ __forceinline__ void dp4a_c32(const C32& w, const C32& q, unsigned& xx, unsigned& qx) {
+  xx = __dp4a(w.a.x, w.a.x, xx); qx = __dp4a(q.a.x, w.a.x, qx);
+  xx = __dp4a(w.a.y, w.a.y, xx); qx = __dp4a(q.a.y, w.a.y, qx);
+  xx = __dp4a(w.a.z, w.a.z, xx); qx = __dp4a(q.a.z, w.a.z, qx);
+  xx = __dp4a(w.a.w, w.a.w, xx); qx = __dp4a(q.a.w, w.a.w, qx);
+  xx = __dp4a(w.b.x, w.b.x, xx); qx = __dp4a(q.b.x, w.b.x, qx);
+  xx = __dp4a(w.b.y, w.b.y, xx); qx = __dp4a(q.b.y, w.b.y, qx);
+  xx = __dp4a(w.b.z, w.b.z, xx); qx = __dp4a(q.b.z, w.b.z, qx);
+  xx = __dp4a(w.b.w, w.b.w, xx); qx = __dp4a(q.b.w, w.b.w, qx);
+}
+
+// rows per lane per pass: AQR_ROWS_PER_PASS 16-byte chunks in flight per lane
+template <int CPL>
+__host__ __device__ constexpr int rows_u() {
+  return AQR_ROWS_PER_PASS / (2 * CPL) < 4 ? 4 : AQR_ROWS_PER_PASS / (2 * CPL) / 4 * 4;
+}
+
+// after reduce_rows, write the row totals r0 + g U + u held by this lane
+template <int LPR, int U>
+__device__ __forceinline__ void store_rows(const int (&part)[U], int r0, int g, int sub, int m, int qq, int32_t* out) {
+  constexpr int PER = U >= LPR ? U / LPR : 1;
+  constexpr int REP = U >= LPR ? 1 : LPR / U;
+#pragma unroll
+  for (int v = 0; v < PER; ++v) {
+    const int u = U >= LPR ? sub * PER + v : sub / REP;
+    const int r = r0 + g * U + u;
+    if ((sub % REP) == 0 && r < m) out[r] = qq + part[v];
+  }
+}
+
 template <int LPR, int CPL>
-__device__ __forceinline__ void list_dists(const IndexView& ix, const uint4 (&qreg)[CPL], int qq,
+__device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg)[CPL], int qq,
                                            const int32_t* ids, int m, int32_t* out, int lane) {
   constexpr int G = 32 / LPR;
-  // all loads of a pass are issued before any is consumed: 16 / CPL rows per lane group, so a
-  // typical layer-0 expansion (<= 64 rows of 128 B) costs ONE DRAM round trip
-  constexpr int U = AQR_ROWS_PER_PASS / CPL;
+  // all loads of a pass are issued before any is consumed: U rows per lane, G * U rows per pass,
+  // so a typical layer-0 expansion (<= 64 rows of 128 B) costs ONE DRAM round trip
+  constexpr int U = rows_u<CPL>();
+  static_assert(U % 4 == 0, "U must be a multiple of 4");
   const int g = lane / LPR, sub = lane % LPR;
-  const int nch = ix.d_pad >> 4;
+  const int nch = ix.d_pad >> 5;
   for (int r0 = 0; r0 < m; r0 += G * U) {
-    uint4 buf[U][CPL];
+    // lane group g owns the U consecutive rows r0 + g U + u: their ids come in U/4 16-byte
+    // shared loads (ids is padded to a whole pass, see make_layout)
+    int idv[U];
+#pragma unroll
+    for (int u4 = 0; u4 < U; u4 += 4) {
+      const int4 t4 = *reinterpret_cast<const int4*>(ids + r0 + g * U + u4);
+      idv[u4] = t4.x;
+      idv[u4 + 1] = t4.y;
+      idv[u4 + 2] = t4.z;
+      idv[u4 + 3] = t4.w;
+    }
+    C32 buf[U][CPL];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int r = r0 + u * G + g;
-      const int id = r < m ? ids[r] : -1;
-      const uint4* row = reinterpret_cast<const uint4*>(ix.codes + (int64_t)(id < 0 ? 0 : id) * ix.d_pad);
+      const int r = r0 + g * U + u;
+      const int id = r < m ? idv[u] : -1;
+      const uint8_t* row = ix.codes + (int64_t)(id < 0 ? 0 : id) * ix.d_pad;
 #pragma unroll
       for (int t = 0; t < CPL; ++t) {
         const int c = sub + LPR * t;
-        buf[u][t] = (id >= 0 && c < nch) ? ldg_stream(row + c) : make_uint4(0, 0, 0, 0);
+        if (id >= 0 && c < nch) {
+          ldg256(row + 32 * c, buf[u][t]);
+        } else {
+          buf[u][t].a = make_uint4(0, 0, 0, 0);
+          buf[u][t].b = make_uint4(0, 0, 0, 0);
+        }
       }
     }
     int part[U];
@@ -226,27 +285,14 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const uint4 (&qr
     for (int u = 0; u < U; ++u) {
       unsigned xx = 0, qx = 0;
 #pragma unroll
-      for (int t = 0; t < CPL; ++t) {
-        const uint4 w = buf[u][t], qw = qreg[t];
-        xx = __dp4a(w.x, w.x, xx); qx = __dp4a(qw.x, w.x, qx);
-        xx = __dp4a(w.y, w.y, xx); qx = __dp4a(qw.y, w.y, qx);
-        xx = __dp4a(w.z, w.z, xx); qx = __dp4a(qw.z, w.z, qx);
-        xx = __dp4a(w.w, w.w, xx); qx = __dp4a(qw.w, w.w, qx);
-      }
+      for (int t = 0; t < CPL; ++t) dp4a_c32(buf[u][t], qreg[t], xx, qx);
       part[u] = (int)xx - 2 * (int)qx;
     }
     // transpose-reduce across the LPR lanes of a row group (U/2 + U/4 + ... shuffles instead of
     // U * log2(LPR)); afterwards lane `sub` holds the total of row u = sub * PER + v in part[v]
     // (U >= LPR), or, when U < LPR, every lane holds the total of row sub / (LPR / U)
     reduce_rows<LPR, U>(part, sub);
-    constexpr int PER = U >= LPR ? U / LPR : 1;
-    constexpr int REP = U >= LPR ? 1 : LPR / U;
-#pragma unroll
-    for (int v = 0; v < PER; ++v) {
-      const int u = U >= LPR ? sub * PER + v : sub / REP;
-      const int r = r0 + u * G + g;
-      if ((sub % REP) == 0 && r < m) out[r] = qq + part[v];
-    }
+    store_rows<LPR, U>(part, r0, g, sub, m, qq, out);
   }
 }
 
@@ -469,23 +515,25 @@ __device__ __forceinline__ void load_query(const IndexView& ix, const float* q, 
 // ------------------------------------------------------------------------------------
 // d^q for the rows of an INLINE block staged in shared memory (rows with id < 0 skipped)
 template <int LPR, int CPL>
-__device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, const uint4 (&qreg)[CPL], int qq,
+__device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, const C32 (&qreg)[CPL], int qq,
                                             const int32_t* ids, int m, int32_t* out, int lane) {
   constexpr int G = 32 / LPR;
-  constexpr int U = CPL == 1 ? 4 : 2;
+  constexpr int U = 4;
   const int g = lane / LPR, sub = lane % LPR;
-  const int nch = d_pad >> 4;
+  const int nch = d_pad >> 5;
   for (int r0 = 0; r0 < m; r0 += G * U) {
-    uint4 buf[U][CPL];
+    C32 buf[U][CPL];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int r = r0 + u * G + g;
+      const int r = r0 + g * U + u;
       const int id = r < m ? ids[r] : -1;
       const uint4* row = reinterpret_cast<const uint4*>(codes_s + (r < m ? r : 0) * d_pad);
 #pragma unroll
       for (int t = 0; t < CPL; ++t) {
         const int c = sub + LPR * t;
-        buf[u][t] = (id >= 0 && c < nch) ? row[c] : make_uint4(0, 0, 0, 0);
+        const bool ok = id >= 0 && c < nch;
+        buf[u][t].a = ok ? row[2 * c] : make_uint4(0, 0, 0, 0);
+        buf[u][t].b = ok ? row[2 * c + 1] : make_uint4(0, 0, 0, 0);
       }
     }
     int part[U];
@@ -493,27 +541,11 @@ __device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, c
     for (int u = 0; u < U; ++u) {
       unsigned xx = 0, qx = 0;
 #pragma unroll
-      for (int t = 0; t < CPL; ++t) {
-        const uint4 w = buf[u][t], qw = qreg[t];
-        xx = __dp4a(w.x, w.x, xx); qx = __dp4a(qw.x, w.x, qx);
-        xx = __dp4a(w.y, w.y, xx); qx = __dp4a(qw.y, w.y, qx);
-        xx = __dp4a(w.z, w.z, xx); qx = __dp4a(qw.z, w.z, qx);
-        xx = __dp4a(w.w, w.w, xx); qx = __dp4a(qw.w, w.w, qx);
-      }
+      for (int t = 0; t < CPL; ++t) dp4a_c32(buf[u][t], qreg[t], xx, qx);
       part[u] = (int)xx - 2 * (int)qx;
     }
-    // transpose-reduce across the LPR lanes of a row group (U/2 + U/4 + ... shuffles instead of
-    // U * log2(LPR)); afterwards lane `sub` holds the total of row u = sub * PER + v in part[v]
-    // (U >= LPR), or, when U < LPR, every lane holds the total of row sub / (LPR / U)
     reduce_rows<LPR, U>(part, sub);
-    constexpr int PER = U >= LPR ? U / LPR : 1;
-    constexpr int REP = U >= LPR ? 1 : LPR / U;
-#pragma unroll
-    for (int v = 0; v < PER; ++v) {
-      const int u = U >= LPR ? sub * PER + v : sub / REP;
-      const int r = r0 + u * G + g;
-      if ((sub % REP) == 0 && r < m) out[r] = qq + part[v];
-    }
+    store_rows<LPR, U>(part, r0, g, sub, m, qq, out);
   }
 }
 
@@ -543,7 +575,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
   uint8_t* blkbuf = wb + L.o_h;
   uint32_t* vhash = c.hbits > 0 ? hash : nullptr;
   const int sub = lane % LPR;
-  const int nch = ix.d_pad >> 4;
+  const int nch = ix.d_pad >> 5;
   const int ef = c.ef;
   uint32_t phase = 0u;
   if (INL) {
@@ -566,11 +598,12 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
 
     // 1. quantize the query
     load_query(ix, q, ld_q, qi, qf, qc, lane);
-    uint4 qreg[CPL];
+    C32 qreg[CPL];
 #pragma unroll
     for (int t = 0; t < CPL; ++t) {
       const int ch = sub + LPR * t;
-      qreg[t] = ch < nch ? reinterpret_cast<const uint4*>(qc)[ch] : make_uint4(0, 0, 0, 0);
+      qreg[t].a = ch < nch ? reinterpret_cast<const uint4*>(qc)[2 * ch] : make_uint4(0, 0, 0, 0);
+      qreg[t].b = ch < nch ? reinterpret_cast<const uint4*>(qc)[2 * ch + 1] : make_uint4(0, 0, 0, 0);
     }
     int qq = 0;
     for (int j = lane; j < ix.d_pad; j += 32) qq += (int)qc[j] * (int)qc[j];
@@ -805,14 +838,19 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
           const int lo = hi - 128 > first_ins ? hi - 128 : first_ins;
           uint64_t v[4];
           int sh[4];
+          // sh(p) = #{c : lb(c) <= p} = #{c : lb(c) < lo} + #{c : lo <= lb(c) <= p}; only the few
+          // candidates whose lb falls inside the group are visited one by one
+          const int base = __popc(__ballot_sync(kFull, lbv < lo));
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             const int p = lo + 32 * t + lane;
             v[t] = p < hi ? W[p] : 0ull;
-            sh[t] = 0;
+            sh[t] = base;
           }
-          for (int j = 0; j < np; ++j) {
-            const int l = __shfl_sync(kFull, lbv, j);
+          uint32_t inside = __ballot_sync(kFull, lbv >= lo && lbv < hi);
+          while (inside) {
+            const int l = __shfl_sync(kFull, lbv, __ffs(inside) - 1);
+            inside &= inside - 1;
 #pragma unroll
             for (int t = 0; t < 4; ++t) sh[t] += l <= lo + 32 * t + lane;
           }
@@ -979,20 +1017,17 @@ size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int wpb) {
 cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                           int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
                           cudaStream_t s) {
-  // lanes per code row: the next power of two >= the row's 16-byte chunks, divided by
-  // AQR_LPR_DIV (each lane then loads CPL chunks of the row), capped at 32
-  const int nch = ix.d_pad >> 4;
-  int p2 = 1;
-  while (p2 < nch) p2 <<= 1;
-  int lpr = p2 / AQR_LPR_DIV;
-  if (lpr < 1) lpr = 1;
+  // lanes per code row: the next power of two >= the row's 32-byte chunks, capped at 32 (each
+  // lane then loads CPL chunks of the row; d <= 2048 gives CPL <= 2)
+  const int nch = ix.d_pad >> 5;
+  int lpr = 1;
+  while (lpr < nch) lpr <<= 1;
   if (lpr > 32) lpr = 32;
   const int cpl = (nch + lpr - 1) / lpr;
   const bool inl = ix.blk != nullptr;
 #define AQR_LAUNCH(L_, C_)                                                                               \
   return inl ? launch_t<L_, C_, true>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)      \
              : launch_t<L_, C_, false>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)
-#if AQR_LPR_DIV == 1
   switch (lpr) {
     case 1: AQR_LAUNCH(1, 1);
     case 2: AQR_LAUNCH(2, 1);
@@ -1002,22 +1037,8 @@ cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* 
     default:
       if (cpl == 1) AQR_LAUNCH(32, 1);
       if (cpl == 2) AQR_LAUNCH(32, 2);
-      if (cpl <= 4) AQR_LAUNCH(32, 4);
       return cudaErrorInvalidValue;
   }
-#else
-  switch (lpr) {
-    case 1: if (cpl == 1) AQR_LAUNCH(1, 1); AQR_LAUNCH(1, 2);
-    case 2: AQR_LAUNCH(2, 2);
-    case 4: AQR_LAUNCH(4, 2);
-    case 8: AQR_LAUNCH(8, 2);
-    case 16: AQR_LAUNCH(16, 2);
-    default:
-      if (cpl <= 2) AQR_LAUNCH(32, 2);
-      if (cpl <= 4) AQR_LAUNCH(32, 4);
-      return cudaErrorInvalidValue;
-  }
-#endif
 #undef AQR_LAUNCH
 }
 
