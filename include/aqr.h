@@ -159,8 +159,7 @@ typedef struct {
  * expansions, 4 upper degree sum, 5 upper evaluations, 6 |C|, 7 re-rank depth, 8 early-term
  * flag, 9 |A|, 10 visited-hash insert failures (re-evaluations allowed by DESIGN.md R15),
  * 11 evaluations below the W threshold, 12 W insertions (11 minus re-evaluations already in
- * W), 13 W buffer flushes, 14 expansions whose node was the smallest unexpanded W entry
- * before the previous expansion's insert (kernel bookkeeping; no oracle counterpart) */
+ * W) (kernel bookkeeping; no oracle counterpart), 13-14 reserved (0) */
 
 /* Optional transcript (all device pointers, each may be NULL).  Per-query arrays are laid
  * out [nq x ...].  Used by the parity tests to compare visit order with the oracle. */

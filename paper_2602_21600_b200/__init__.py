@@ -20,7 +20,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 AQR_L2, AQR_IP = 0, 1
 NCOUNT = 15
 COUNTER_NAMES = ["expansions", "deg_sum", "evals", "upper_exp", "upper_deg_sum", "upper_evals", "n_coarse",
-                 "depth", "early_term", "n_asym", "hash_fail", "below_thr", "w_inserts", "w_flushes", "next_guess_hits"]
+                 "depth", "early_term", "n_asym", "hash_fail", "below_thr", "w_inserts", "reserved13", "reserved14"]
 
 
 class AqrError(RuntimeError):

@@ -49,11 +49,17 @@ def _dist():
     return dist
 
 
+def _world(group=None) -> int:
+    """World size, 1 when no process group is initialised (a single-GPU run)."""
+    d = _dist()
+    return d.get_world_size(group) if d.is_available() and d.is_initialized() else 1
+
+
 def all_gather_lists(dist_t, ids_t, group=None):
     """[nq, k] dists (fp32) + ids (int32) of every rank -> [world, nq, k] each, rank order."""
     import torch
     d = _dist()
-    world = d.get_world_size(group)
+    world = _world(group)
     if world == 1:
         return dist_t.unsqueeze(0), ids_t.unsqueeze(0)
     nq, k = dist_t.shape
@@ -81,7 +87,7 @@ def gather_rows(t, group=None):
     """Concatenate per-rank row blocks (possibly of different lengths) in rank order."""
     import torch
     d = _dist()
-    world = d.get_world_size(group)
+    world = _world(group)
     if world == 1:
         return t
     n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)

@@ -89,3 +89,15 @@ def test_partitions():
     assert [P.shard_rows(10_000_000, 8, s) for s in (0, 7)] == [(0, 1_250_000), (8_750_000, 10_000_000)]
     with pytest.raises(ValueError):
         P.shards_of_rank(8, 3, 0)
+
+
+def test_single_process_without_group():
+    """A single-GPU run never initialises a process group: the plumbing is the identity."""
+    assert not dist.is_initialized()
+    d = torch.arange(6, dtype=torch.float32).reshape(2, 3)
+    i = torch.arange(6, dtype=torch.int32).reshape(2, 3)
+    gd, gi = P.gather_merge(d, i, _merge)
+    assert gd is d and gi is i
+    assert P.gather_rows(i) is i
+    od, oi = P.all_gather_lists(d, i)
+    assert od.shape == (1, 2, 3) and oi.shape == (1, 2, 3)
