@@ -35,6 +35,9 @@ EF_GRID = [16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 640, 768, 896, 1024,
 # fixed HNSW construction inputs of BASELINE.json
 P_MAX = {"C1": 5.0, "C2": 0.2, "C3": 5.0, "C4": 5.0, "C5": 5.0}
 TARGET_RECALL = 0.98
+# the ef our arm reports (smallest ef with recall@10 >= 0.98, measured, profiles/r01): the
+# reference arm (the oracle) is timed on the same point; configs without one use BJ's ef
+EF_AT_TARGET = {"C1": 64, "C2": 784, "C3": 1536, "C4": 128, "C5": 128}
 LAYOUT = "auto"
 BUILD_FLAGS = 1  # host builder: Malkov's keepPrunedConnections (R14)
 
@@ -654,7 +657,7 @@ def run_reference(args):
     g = G.build_hnsw(codes, M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg=cfg), args.threads,
                      flags=BUILD_FLAGS)
     log(f"[reference] index built in {time.time() - t0:.1f} s")
-    ef = 256 if args.ef == "auto" else int(args.ef)
+    ef = EF_AT_TARGET.get(cfg, 256) if args.ef == "auto" else int(args.ef)
     m = G_ef_mapping(ef, k)
     oix = oracle.Index(w.x, codes, quant, g, w.metric)
     t0 = time.time()
