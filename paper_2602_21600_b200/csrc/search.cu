@@ -125,42 +125,47 @@ __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t 
 // per-warp shared-memory layout
 // ------------------------------------------------------------------------------------
 struct Layout {
-  int o_qc, o_qf, o_w, o_h, o_s23, o_nb, o_nd, o_cand, o_cs, o_lb, o_bar, per_warp;
+  // runtime part of the per-warp layout; the hot arrays of the beam (Hot<> below) sit at
+  // compile-time offsets before W, so every access to them is [warp base + immediate]
+  int o_w, o_qc, o_qf, o_h, o_s23, per_warp;
   int region;     // bytes of the hash / block-buffer region (reused by Stage 2/3)
   int buf_bytes;  // INLINE: one staged block (128-byte aligned)
 };
 
-__host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
+__host__ __device__ constexpr int al16(int x) { return (x + 15) & ~15; }
 
-Layout make_layout(const IndexView& ix, const SearchCfg& c) {
+// rows per lane per list_dists pass: AQR_ROWS_PER_PASS 16-byte chunks in flight per lane
+template <int CPL>
+__host__ __device__ constexpr int rows_u() {
+  return AQR_ROWS_PER_PASS / (2 * CPL) < 4 ? 4 : AQR_ROWS_PER_PASS / (2 * CPL) / 4 * 4;
+}
+
+// the beam's per-warp scratch for adjacency rows of up to CAP entries (CAP = 64 or 160)
+template <int LPR, int CPL, int CAP>
+struct Hot {
+  static constexpr int PASS = (32 / LPR) * rows_u<CPL>();  // rows read per list_dists pass
+  static constexpr int NB1 = (CAP + PASS - 1) / PASS * PASS;
+  static constexpr int NB = NB1 > (CAP + 31) / 32 * 32 ? NB1 : (CAP + 31) / 32 * 32;
+  static constexpr int o_nb = 0;                            // int32 [NB] neighbour ids
+  static constexpr int o_nd = o_nb + al16(4 * NB);          // int32 [CAP] d^q
+  static constexpr int o_cand = o_nd + al16(4 * CAP);       // u64 [CAP] new W keys
+  static constexpr int o_cs = o_cand + 8 * CAP;             // u64 [CAP] survivors / sorted keys
+  static constexpr int o_lb = o_cs + 8 * CAP;               // int32 [CAP] W lower bounds
+  static constexpr int o_bar = o_lb + al16(4 * CAP);        // mbarrier (INLINE)
+  static constexpr int bytes = o_bar + 16;                  // W follows
+};
+
+Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   Layout L;
-  int o = 0;
+  int o = hot_bytes;
+  L.o_w = o; o += al16(8 * (c.ef + 1));
   L.o_qc = o; o += al16(ix.d_pad);
   L.o_qf = o; o += al16(4 * ix.d4);
-  L.o_w = o; o += al16(8 * (c.ef + 1));
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
   L.region = ix.blk ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
   o = (o + 127) & ~127;
   L.o_h = o; o += al16(L.region);
   L.o_s23 = o; o += c.ef >= 2 * c.n_coarse ? 0 : al16(8 * c.n_coarse);
-  // nb is read in whole list_dists passes (G * U rows, the same LPR / CPL choice as
-  // launch_search), so it is padded to one
-  {
-    const int nch = ix.d_pad >> 5;
-    int lpr = 1;
-    while (lpr < nch) lpr <<= 1;
-    if (lpr > 32) lpr = 32;
-    const int cpl = (nch + lpr - 1) / lpr;
-    const int u = AQR_ROWS_PER_PASS / (2 * cpl) < 4 ? 4 : AQR_ROWS_PER_PASS / (2 * cpl) / 4 * 4;
-    const int pass = (32 / lpr) * u;
-    const int rows = (ix.ld0 + pass - 1) / pass * pass;
-    L.o_nb = o; o += al16(4 * (rows > ix.M ? rows : ix.M));
-  }
-  L.o_nd = o; o += al16(4 * ix.ld0);
-  L.o_cand = o; o += al16(8 * ix.ld0);
-  L.o_cs = o; o += al16(8 * ix.ld0);
-  L.o_lb = o; o += al16(4 * ix.ld0);
-  L.o_bar = o; o += 16;
   L.per_warp = (o + 127) & ~127;
   return L;
 }
@@ -222,11 +227,6 @@ __device__ __forceinline__ void dp4a_c32(const C32& w, const C32& q, unsigned& x
   xx = __dp4a(w.b.w, w.b.w, xx); qx = __dp4a(q.b.w, w.b.w, qx);
 }
 
-// rows per lane per pass: AQR_ROWS_PER_PASS 16-byte chunks in flight per lane
-template <int CPL>
-__host__ __device__ constexpr int rows_u() {
-  return AQR_ROWS_PER_PASS / (2 * CPL) < 4 ? 4 : AQR_ROWS_PER_PASS / (2 * CPL) / 4 * 4;
-}
 
 // after reduce_rows, write the row totals r0 + g U + u held by this lane
 template <int LPR, int U>
@@ -554,24 +554,25 @@ __device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, c
 // next block prefetched during the merge) or the GATHER layout (row + per-code gathers,
 // shared-memory visited hash)
 // ------------------------------------------------------------------------------------
-template <int LPR, int CPL, bool INL>
+template <int LPR, int CPL, bool INL, int CAP>
 __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_kernel(IndexView ix, SearchCfg c, Layout L, const float* __restrict__ q,
                                                      int64_t nq, int64_t ld_q, int32_t* __restrict__ out_ids,
                                                      float* __restrict__ out_dist, aqr_debug dbg, int has_dbg,
                                                      int* __restrict__ counter) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
+  using H = Hot<LPR, CPL, CAP>;
   uint8_t* wb = smem + (threadIdx.x >> 5) * L.per_warp;
   uint8_t* qc = wb + L.o_qc;
   float* qf = reinterpret_cast<float*>(wb + L.o_qf);
-  uint64_t* W = reinterpret_cast<uint64_t*>(wb + L.o_w);
+  uint64_t* W = reinterpret_cast<uint64_t*>(wb + H::bytes);
   uint32_t* hash = reinterpret_cast<uint32_t*>(wb + L.o_h);
-  int32_t* nb = reinterpret_cast<int32_t*>(wb + L.o_nb);
-  int32_t* nd = reinterpret_cast<int32_t*>(wb + L.o_nd);
-  uint64_t* cand = reinterpret_cast<uint64_t*>(wb + L.o_cand);
-  uint64_t* cs = reinterpret_cast<uint64_t*>(wb + L.o_cs);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wb + L.o_bar);
-  int32_t* clb = reinterpret_cast<int32_t*>(wb + L.o_lb);
+  int32_t* nb = reinterpret_cast<int32_t*>(wb + H::o_nb);
+  int32_t* nd = reinterpret_cast<int32_t*>(wb + H::o_nd);
+  uint64_t* cand = reinterpret_cast<uint64_t*>(wb + H::o_cand);
+  uint64_t* cs = reinterpret_cast<uint64_t*>(wb + H::o_cs);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wb + H::o_bar);
+  int32_t* clb = reinterpret_cast<int32_t*>(wb + H::o_lb);
   uint8_t* blkbuf = wb + L.o_h;
   uint32_t* vhash = c.hbits > 0 ? hash : nullptr;
   const int sub = lane % LPR;
@@ -821,53 +822,11 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         cursor = pos + 1;
         continue;
       }
-      // merge: candidate c lands at lb(c) + rank(c) (lb = #W keys below it, from the filter; rank =
-      // #candidates below it); an old entry W[p] moves right by #{c : lb(c) <= p}
-      if (np <= 32) {
-        // the usual case: candidates held one per lane; the shift amounts come from shuffles, so
-        // each group of 4 chunks is one batch of independent loads, then one batch of stores
-        const bool act = lane < np;
-        const uint64_t kk = act ? cand[lane] : ~0ull;
-        const int lbv = act ? clb[lane] : INT_MAX;
-        int rk = 0;
-        for (int j = 0; j < np; ++j) rk += shfl_u64(kk, j) < kk;
-        int first_ins = lbv;
-#pragma unroll
-        for (int off = 16; off; off >>= 1) first_ins = min(first_ins, __shfl_xor_sync(kFull, first_ins, off));
-        for (int hi = size; hi > first_ins; hi -= 128) {
-          const int lo = hi - 128 > first_ins ? hi - 128 : first_ins;
-          uint64_t v[4];
-          int sh[4];
-          // sh(p) = #{c : lb(c) <= p} = #{c : lb(c) < lo} + #{c : lo <= lb(c) <= p}; only the few
-          // candidates whose lb falls inside the group are visited one by one
-          const int base = __popc(__ballot_sync(kFull, lbv < lo));
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int p = lo + 32 * t + lane;
-            v[t] = p < hi ? W[p] : 0ull;
-            sh[t] = base;
-          }
-          uint32_t inside = __ballot_sync(kFull, lbv >= lo && lbv < hi);
-          while (inside) {
-            const int l = __shfl_sync(kFull, lbv, __ffs(inside) - 1);
-            inside &= inside - 1;
-#pragma unroll
-            for (int t = 0; t < 4; ++t) sh[t] += l <= lo + 32 * t + lane;
-          }
-          __syncwarp();
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int p = lo + 32 * t + lane;
-            if (p < hi && p + sh[t] < ef) W[p + sh[t]] = v[t];
-          }
-          __syncwarp();
-        }
-        if (act && lbv + rk < ef) W[lbv + rk] = kk;
-        __syncwarp();
-        size = size + np < ef ? size + np : ef;
-        cursor = first_ins < pos + 1 ? first_ins : pos + 1;
-        continue;
-      }
+      // merge: sort the new keys (rank = #new keys below) into cs / slb; new key j lands at
+      // slb[j] + j, and the old entries between consecutive insertion points, the segment
+      // W[slb[j], slb[j+1]) (slb[np] = size), move right by j + 1 -- a constant per segment, so
+      // each segment is a plain block move (top segment and top chunks first, in place; groups of
+      // 4 chunks: one batch of loads, then one of stores).  Entries pushed to >= ef drop out.
       int32_t* slb = reinterpret_cast<int32_t*>(nd);
       for (int i = lane; i < np; i += 32) {
         const uint64_t kk = cand[i];
@@ -878,26 +837,30 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       }
       __syncwarp();
       const int first_ins = slb[0];
-      // shift the old entries W[first_ins:size) right, top chunk first (in place).  Entry i moves
-      // by sh(i) = #{r : slb[r] <= i}; walking down, r_hi tracks #{r : slb[r] <= hi - 1} and only
-      // the few candidates whose slb falls inside the chunk adjust individual lanes, so the whole
-      // shift costs O(chunks + np) uniform steps instead of a search per entry
-      int r_hi = np;
-      for (int hi = size; hi > first_ins; hi -= 32) {
-        const int lo = hi - 32 > first_ins ? hi - 32 : first_ins;
-        while (r_hi > 0 && slb[r_hi - 1] > hi - 1) --r_hi;
-        const int i = lo + lane;
-        int sh = r_hi;
-        for (int r = r_hi; r > 0 && slb[r - 1] > lo; --r) sh -= slb[r - 1] > i;
-        uint64_t v = 0;
-        if (i < hi) v = W[i];
-        __syncwarp();
-        if (i < hi && i + sh < ef) W[i + sh] = v;
-        __syncwarp();
+      int seg_hi = size;
+      for (int j = np - 1; j >= 0; --j) {
+        const int sh = j + 1;
+        const int seg_lo = slb[j];
+        for (int hi = seg_hi < ef - sh ? seg_hi : ef - sh; hi > seg_lo; hi -= 128) {
+          const int lo = hi - 128 > seg_lo ? hi - 128 : seg_lo;
+          uint64_t v[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int p = lo + 32 * t + lane;
+            v[t] = p < hi ? W[p] : 0ull;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int p = lo + 32 * t + lane;
+            if (p < hi) W[p + sh] = v[t];
+          }
+          __syncwarp();
+        }
+        seg_hi = seg_lo;
       }
-      for (int i = lane; i < np; i += 32) {
-        const int dst = slb[i] + i;
-        if (dst < ef) W[dst] = cs[i];
+      for (int j = lane; j < np; j += 32) {
+        if (slb[j] + j < ef) W[slb[j] + j] = cs[j];
       }
       __syncwarp();
       size = size + np < ef ? size + np : ef;
@@ -983,13 +946,13 @@ __global__ void __launch_bounds__(128) rerank_kernel(IndexView ix, SearchCfg c, 
   finish_query(ix, cc, qf, cid, nullptr, nc, akeys, rkeys, qi, out_ids, out_dist, none, false, lane, nullptr);
 }
 
-template <int LPR, int CPL, bool INL>
+template <int LPR, int CPL, bool INL, int CAP>
 cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                      int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
                      cudaStream_t s) {
-  const Layout L = make_layout(ix, c);
+  const Layout L = make_layout(ix, c, Hot<LPR, CPL, CAP>::bytes);
   const size_t smem = (size_t)L.per_warp * wpb;
-  auto kern = search_kernel<LPR, CPL, INL>;
+  auto kern = search_kernel<LPR, CPL, INL, CAP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
@@ -1008,38 +971,57 @@ cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, in
   return cudaGetLastError();
 }
 
+// lanes per code row: the next power of two >= the row's 32-byte chunks, capped at 32 (each lane
+// then loads CPL chunks of the row; d <= 2048 gives CPL <= 2); CAP: the adjacency-row class
+struct Shape {
+  int lpr, cpl, cap;
+};
+Shape shape_of(const IndexView& ix) {
+  const int nch = ix.d_pad >> 5;
+  int lpr = 1;
+  while (lpr < nch) lpr <<= 1;
+  if (lpr > 32) lpr = 32;
+  return Shape{lpr, (nch + lpr - 1) / lpr, ix.cap0 <= 64 ? 64 : 160};
+}
+
+// F(lpr, cpl, cap) dispatch over the instantiated shapes
+#define AQR_DISPATCH(SH, CALL)                                                      \
+  switch ((SH).lpr * 1000 + (SH).cpl * 200 + (SH).cap) {                           \
+    case 1264: CALL(1, 1, 64); case 1360: CALL(1, 1, 160);                        \
+    case 2264: CALL(2, 1, 64); case 2360: CALL(2, 1, 160);                        \
+    case 4264: CALL(4, 1, 64); case 4360: CALL(4, 1, 160);                        \
+    case 8264: CALL(8, 1, 64); case 8360: CALL(8, 1, 160);                        \
+    case 16264: CALL(16, 1, 64); case 16360: CALL(16, 1, 160);                    \
+    case 32264: CALL(32, 1, 64); case 32360: CALL(32, 1, 160);                    \
+    case 32464: CALL(32, 2, 64); case 32560: CALL(32, 2, 160);                    \
+    default: break;                                                                \
+  }
+
+int hot_bytes(const IndexView& ix) {
+#define AQR_HOT(L_, C_, K_) return Hot<L_, C_, K_>::bytes
+  AQR_DISPATCH(shape_of(ix), AQR_HOT)
+#undef AQR_HOT
+  return -1;
+}
+
 }  // namespace
 
 size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int wpb) {
-  return (size_t)make_layout(ix, c).per_warp * wpb;
+  const int hb = hot_bytes(ix);
+  if (hb < 0) return ~(size_t)0;
+  return (size_t)make_layout(ix, c, hb).per_warp * wpb;
 }
 
 cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                           int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
                           cudaStream_t s) {
-  // lanes per code row: the next power of two >= the row's 32-byte chunks, capped at 32 (each
-  // lane then loads CPL chunks of the row; d <= 2048 gives CPL <= 2)
-  const int nch = ix.d_pad >> 5;
-  int lpr = 1;
-  while (lpr < nch) lpr <<= 1;
-  if (lpr > 32) lpr = 32;
-  const int cpl = (nch + lpr - 1) / lpr;
   const bool inl = ix.blk != nullptr;
-#define AQR_LAUNCH(L_, C_)                                                                               \
-  return inl ? launch_t<L_, C_, true>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)      \
-             : launch_t<L_, C_, false>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)
-  switch (lpr) {
-    case 1: AQR_LAUNCH(1, 1);
-    case 2: AQR_LAUNCH(2, 1);
-    case 4: AQR_LAUNCH(4, 1);
-    case 8: AQR_LAUNCH(8, 1);
-    case 16: AQR_LAUNCH(16, 1);
-    default:
-      if (cpl == 1) AQR_LAUNCH(32, 1);
-      if (cpl == 2) AQR_LAUNCH(32, 2);
-      return cudaErrorInvalidValue;
-  }
+#define AQR_LAUNCH(L_, C_, K_)                                                                            \
+  return inl ? launch_t<L_, C_, true, K_>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)    \
+             : launch_t<L_, C_, false, K_>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)
+  AQR_DISPATCH(shape_of(ix), AQR_LAUNCH)
 #undef AQR_LAUNCH
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_build_inline(const IndexView& ix, uint8_t* blk, cudaStream_t s) {
