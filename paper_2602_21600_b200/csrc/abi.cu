@@ -169,7 +169,8 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   int32_t* a0 = (int32_t*)alloc(sizeof(int32_t) * (size_t)n * V.ld0);
   int32_t* au = (int32_t*)alloc(sizeof(int32_t) * (size_t)(D.upper_rows > 0 ? D.upper_rows * M : 1));
   int32_t* uo = (int32_t*)alloc(sizeof(int32_t) * (size_t)n);
-  if (!codes || !base || !mn || !sc || !a0 || !au || !uo) {
+  int32_t* xn = (int32_t*)alloc(sizeof(int32_t) * (size_t)n);
+  if (!codes || !base || !mn || !sc || !a0 || !au || !uo || !xn) {
     set_error("aqr: upload: device allocation failed");
     return fail(AQR_E_OOM);
   }
@@ -197,12 +198,19 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
     return fail(st);
   }
   V.codes = codes;
+  V.xnorm = xn;
   V.base = base;
   V.min_j = mn;
   V.scale_j = sc;
   V.adj0 = a0;
   V.adj_up = au;
   V.up_off = uo;
+  e = aqr::launch_code_norms(V, xn, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    aqr_status st = cuda_fail(e, "upload: code norms");
+    return fail(st);
+  }
   V.blk = nullptr;
   V.blk_ids = round_up(4 * cap0, 16);
   V.blk_bytes = V.blk_ids + cap0 * V.d_pad;

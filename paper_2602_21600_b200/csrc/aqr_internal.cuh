@@ -15,6 +15,7 @@ struct IndexView {
   int32_t d, d_pad, d4, metric;
   int64_t id_base;
   const uint8_t* codes;   // [n x d_pad]
+  const int32_t* xnorm;   // [n] sum of squared codes |x^|^2 (d^q = |q^|^2 + |x^|^2 - 2 q^.x^)
   const float* base;      // [n x d4]   (d4 = round_up(d, 4), zero padded)
   const float* min_j;     // [d4]       (padding: 0)
   const float* scale_j;   // [d4]       (padding: 1)
@@ -59,5 +60,6 @@ cudaError_t launch_merge(const float* dist, const int32_t* ids, int32_t n_lists,
                          float* out_dist, int32_t* out_ids, cudaStream_t s);
 size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int warps_per_block);
 cudaError_t launch_build_inline(const IndexView& ix, uint8_t* blk, cudaStream_t s);
+cudaError_t launch_code_norms(const IndexView& ix, int32_t* out, cudaStream_t s);
 
 }  // namespace aqr

@@ -115,7 +115,7 @@ __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t 
   int lo = 0, hi = n;
   while (lo < hi) {
     int mid = (lo + hi) >> 1;
-    if ((a[mid] & ~1ull) < key) lo = mid + 1;
+    if (a[mid] < key) lo = mid + 1;  // key has flag 0 and keys differ above bit 0: no mask needed
     else hi = mid;
   }
   return lo;
@@ -227,6 +227,17 @@ __device__ __forceinline__ void dp4a_c32(const C32& w, const C32& q, unsigned& x
   xx = __dp4a(w.b.w, w.b.w, xx); qx = __dp4a(q.b.w, w.b.w, qx);
 }
 
+__device__ __forceinline__ void dp4a_qx(const C32& w, const C32& q, unsigned& qx) {
+  qx = __dp4a(q.a.x, w.a.x, qx);
+  qx = __dp4a(q.a.y, w.a.y, qx);
+  qx = __dp4a(q.a.z, w.a.z, qx);
+  qx = __dp4a(q.a.w, w.a.w, qx);
+  qx = __dp4a(q.b.x, w.b.x, qx);
+  qx = __dp4a(q.b.y, w.b.y, qx);
+  qx = __dp4a(q.b.z, w.b.z, qx);
+  qx = __dp4a(q.b.w, w.b.w, qx);
+}
+
 
 // after reduce_rows, write the row totals r0 + g U + u held by this lane
 template <int LPR, int U>
@@ -263,6 +274,18 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg
       idv[u4 + 2] = t4.z;
       idv[u4 + 3] = t4.w;
     }
+    // |x^|^2 (precomputed per node) of the rows whose totals this lane holds after the reduction;
+    // d^q = |q^|^2 + |x^|^2 - 2 q^.x^ then needs dp4a only for q^.x^
+    constexpr int PER = U >= LPR ? U / LPR : 1;
+    constexpr int REP = U >= LPR ? 1 : LPR / U;
+    int xn[PER];
+#pragma unroll
+    for (int v = 0; v < PER; ++v) {
+      const int u = U >= LPR ? sub * PER + v : sub / REP;
+      const int r = r0 + g * U + u;
+      const int id = r < m ? ids[r] : -1;
+      xn[v] = id >= 0 ? __ldg(ix.xnorm + id) : 0;
+    }
     C32 buf[U][CPL];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -283,15 +306,17 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg
     int part[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      unsigned xx = 0, qx = 0;
+      unsigned qx = 0;
 #pragma unroll
-      for (int t = 0; t < CPL; ++t) dp4a_c32(buf[u][t], qreg[t], xx, qx);
-      part[u] = (int)xx - 2 * (int)qx;
+      for (int t = 0; t < CPL; ++t) dp4a_qx(buf[u][t], qreg[t], qx);
+      part[u] = -2 * (int)qx;
     }
     // transpose-reduce across the LPR lanes of a row group (U/2 + U/4 + ... shuffles instead of
     // U * log2(LPR)); afterwards lane `sub` holds the total of row u = sub * PER + v in part[v]
     // (U >= LPR), or, when U < LPR, every lane holds the total of row sub / (LPR / U)
     reduce_rows<LPR, U>(part, sub);
+#pragma unroll
+    for (int v = 0; v < PER; ++v) part[v] += xn[v];
     store_rows<LPR, U>(part, r0, g, sub, m, qq, out);
   }
 }
@@ -897,6 +922,22 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
   }
 }
 
+// |x^|^2 per node (exact int32: <= 255^2 * 2048 < 2^31), one thread per code row
+__global__ void code_norms_kernel(IndexView ix, int32_t* __restrict__ out) {
+  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= ix.n) return;
+  const uint4* row = reinterpret_cast<const uint4*>(ix.codes + v * ix.d_pad);
+  unsigned acc = 0;
+  for (int c = 0; c < (ix.d_pad >> 4); ++c) {
+    const uint4 w = row[c];
+    acc = __dp4a(w.x, w.x, acc);
+    acc = __dp4a(w.y, w.y, acc);
+    acc = __dp4a(w.z, w.z, acc);
+    acc = __dp4a(w.w, w.w, acc);
+  }
+  out[v] = (int32_t)acc;
+}
+
 // INLINE layout builder: one warp per node copies its ids and its neighbours' code rows
 __global__ void build_inline_kernel(IndexView ix, uint8_t* __restrict__ blk) {
   const int lane = threadIdx.x & 31;
@@ -1022,6 +1063,12 @@ cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* 
   AQR_DISPATCH(shape_of(ix), AQR_LAUNCH)
 #undef AQR_LAUNCH
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_code_norms(const IndexView& ix, int32_t* out, cudaStream_t s) {
+  const int64_t grid = (ix.n + 255) / 256;
+  code_norms_kernel<<<(unsigned)grid, 256, 0, s>>>(ix, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_build_inline(const IndexView& ix, uint8_t* blk, cudaStream_t s) {
