@@ -205,7 +205,7 @@ def build_index(w, cfg, rank, world, threads):
     return x, codes, quant, g, ix, info
 
 
-def bytes_per_query(tot, nq, d, k, distinct_ratio=1.0):
+def bytes_per_query(tot, nq, d, k, distinct_ratio=1.0, traversal="aqr"):
     """Algorithmic bytes from the kernel counters:
     query 4d + adjacency 4(deg+1) per expansion (all layers) + d per DISTINCT code evaluation
     (all layers) + N_c d (Stage 2 re-read) + 4d per exact re-rank + 8k output.  The kernel
@@ -213,6 +213,10 @@ def bytes_per_query(tot, nq, d, k, distinct_ratio=1.0):
     evaluations / neighbours scored, measured exactly by the oracle (same visit order) on a query
     sample, converts that count to the algorithmic one."""
     exp, deg, ev, uexp, udeg, uev, nc, depth, et, na, fails = [float(v) for v in tot[:11]]
+    if traversal == "fp32":  # the baseline reads a 4d-byte fp32 row per distinct evaluation, no re-rank
+        b = (4 * d * nq + 4 * (deg + exp) + 4 * (udeg + uexp) + 4 * d * ((ev - fails) * distinct_ratio + uev)
+             + 8 * k * nq)
+        return b / nq
     b = (4 * d * nq + 4 * (deg + exp) + 4 * (udeg + uexp) + d * ((ev - fails) * distinct_ratio + uev) + d * nc
          + 4 * d * depth + 8 * k * nq)
     return b / nq
@@ -231,9 +235,9 @@ def oracle_index(w, cfg, codes, g):
     return oracle.Index(w.x, o_codes, o_quant, g, w.metric), codes_equal, time.time() - t0
 
 
-def distinct_ratio_from_oracle(oix, w, m, k, n_sample=256):
+def distinct_ratio_from_oracle(oix, w, m, k, n_sample=256, traversal="aqr"):
     import oracle
-    _, _, tr = oracle.search(oix, w.q[:n_sample], k, trace=True, exp_cap=1, **m)
+    _, _, tr = oracle.search(oix, w.q[:n_sample], k, trace=True, exp_cap=1, traversal=traversal, **m)
     cnt = tr["counters"].sum(0)
     # layer-0 distinct evaluations / layer-0 neighbours seen (oracle counters 2 and 1)
     return float(cnt[2]) / max(float(cnt[1]), 1.0), int(len(w.q[:n_sample]))
@@ -271,13 +275,15 @@ def run_aqr(args):
         # "preset": Table 3 "0.97+" (R13); "full": the same N_c with every C entry re-ranked
         # exactly (N_rerank = N_c) -- the Fig. 3 knob for data where d^q / d^a order is noisy (R20)
         mm = aqr.ef_mapping(ef, k)
+        if args.traversal == "fp32":  # the baseline: W's first k are the result
+            return dict(ef=max(ef, k), n_coarse=k, n_rerank=k)
         if mode == "full":
             mm["n_rerank"] = mm["n_coarse"]
         return mm
 
     def measure(ef, mode):
         m = mapping(ef, mode)
-        p = aqr.make_params(k, **m, visited_bits=args.vbits[0])
+        p = aqr.make_params(k, **m, visited_bits=args.vbits[0], traversal=args.traversal)
         s = aqr.Searcher(ix, len(q), p)
         s.run(q)
         torch.cuda.synchronize()
@@ -341,7 +347,7 @@ def run_aqr(args):
     vb_results = []
     best_vb, best_ms = 0, float("inf")
     for vb in args.vbits:
-        p = aqr.make_params(k, **m, visited_bits=vb)
+        p = aqr.make_params(k, **m, visited_bits=vb, traversal=args.traversal)
         s = aqr.Searcher(ix, len(q), p)
         s.run(q)
         torch.cuda.synchronize()
@@ -357,7 +363,7 @@ def run_aqr(args):
             best_vb, best_ms = vb, ms
     if rank == 0 and len(args.vbits) > 1:
         log(f"[bench] visited_bits sweep {vb_results} -> {best_vb}")
-    p = aqr.make_params(k, **m, visited_bits=best_vb)
+    p = aqr.make_params(k, **m, visited_bits=best_vb, traversal=args.traversal)
     s = aqr.Searcher(ix, len(q), p)
     # counters for the roofline (separate, untimed run with the stats path)
     s.totals.zero_()
@@ -368,9 +374,9 @@ def run_aqr(args):
     ratio, n_ratio = 1.0, 0
     if rank == 0 and not args.no_oracle:
         oix, codes_equal, t_otrain = oracle_index(w, cfg, codes, g)
-        ratio, n_ratio = distinct_ratio_from_oracle(oix, w, m, k)
+        ratio, n_ratio = distinct_ratio_from_oracle(oix, w, m, k, traversal=args.traversal)
     ratio = float(allreduce_sum([ratio if rank == 0 else 0.0], world)[0]) if world > 1 else ratio
-    bq = bytes_per_query(tot_counters, len(q), w.x.shape[1], k, ratio)
+    bq = bytes_per_query(tot_counters, len(q), w.x.shape[1], k, ratio, args.traversal)
 
     # ---- device-timed region: W warm-up steps, then K steps bracketed by barrier + sync ----
     stream = torch.cuda.current_stream()
@@ -449,7 +455,7 @@ def run_aqr(args):
     # ---- CPU oracle baseline: rank 0, N = 1, bounded query sample ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and oix is not None:
-        cpu = cpu_baseline(w, oix, m, k, args.cpu_seconds, s)
+        cpu = cpu_baseline(w, oix, m, k, args.cpu_seconds, s, args.traversal)
         cpu["codes_equal_full_size"] = codes_equal
         cpu["oracle_train_s"] = round(t_otrain, 1)
 
@@ -461,7 +467,7 @@ def run_aqr(args):
             "data": "synthetic (seeded, BASELINE.json config recipe; paper datasets unavailable)",
             "config": {"workload": f"{cfg}: {len(w.x)} x {w.x.shape[1]} {w.metric}, {nq} queries, k={k}",
                        "ef": chosen, "n_coarse": m["n_coarse"], "n_rerank": m["n_rerank"],
-                       "rerank": chosen_mode,
+                       "rerank": chosen_mode, "traversal": args.traversal,
                        "recall@10": next((z["recall"] for z in sweep if z["ef"] == chosen and z["rerank"] == chosen_mode),
                                          None),
                        "visited_bits": best_vb, "visited_bits_sweep": vb_results, "queries_per_rank": len(q), "parallelism": f"replicated index, dp{world}",
@@ -486,16 +492,16 @@ def run_aqr(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(w, oix, m, k, seconds, searcher):
+def cpu_baseline(w, oix, m, k, seconds, searcher, traversal="aqr"):
     """The CPU oracle as it stands, single thread, on a bounded sample of the same queries."""
     import oracle
     n_try = 8
     t0 = time.time()
-    oracle.search(oix, w.q[:n_try], k, **m)
+    oracle.search(oix, w.q[:n_try], k, traversal=traversal, **m)
     per_q = (time.time() - t0) / n_try
     n_s = int(max(n_try, min(len(w.q), seconds / max(per_q, 1e-6))))
     t0 = time.time()
-    o_ids, _ = oracle.search(oix, w.q[:n_s], k, **m)
+    o_ids, _ = oracle.search(oix, w.q[:n_s], k, traversal=traversal, **m)
     el = time.time() - t0
     g_ids = searcher.ids[:n_s].cpu().numpy()
     return {"value": round(n_s / el, 2), "unit": "queries/s", "cores": 1, "kind": "oracle",
@@ -720,8 +726,11 @@ def main():
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--ef", default="auto")
     ap.add_argument("--full-sweep", action="store_true")
-    ap.add_argument("--rerank", default="preset,full",
-                    help="re-rank depth mappings swept: preset (Table 3, N_rerank = 28) and/or full (N_rerank = N_c)")
+    ap.add_argument("--traversal", default="aqr", choices=["aqr", "fp32"],
+                    help="aqr: the method; fp32: the paper's baseline HNSW search on the same graph (NEXT-2)")
+    ap.add_argument("--rerank", default="auto",
+                    help="re-rank depth mappings swept: preset (Table 3, N_rerank = 28) and/or full (N_rerank = N_c); "
+                         "auto = preset for C1/C2 (identical recall there, measured), preset,full for C3/C4")
     ap.add_argument("--vbits", type=lambda v: [int(t) for t in v.split(",")], default=[-1],
                     help="visited-hash sizes (log2 slots, 0 = auto) tried at the chosen ef; fastest is timed")
     ap.add_argument("--threads", type=int, default=0)
@@ -737,6 +746,8 @@ def main():
     if args.warmup < 3:
         log("[bench] warm-up raised to 3 (timing rule)")
         args.warmup = 3
+    if args.rerank == "auto":
+        args.rerank = "preset,full" if args.config in ("C3", "C4") else "preset"
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "C5":

@@ -152,7 +152,15 @@ typedef struct {
                            6..16; 0 or -1 = no visited set (default): re-encountered nodes are
                            re-scored and dropped by the W dedupe (R15).  INLINE: ignored. */
   int32_t warps_per_block; /* reserved, must be 0 (the CTA shape is fixed at compile time) */
+  int32_t traversal;    /* AQR_TRAVERSAL_AQR (0): the method (Alg2).  AQR_TRAVERSAL_FP32 (1): the
+                           paper's baseline (plain HNSW search) on the same graph: greedy
+                           descent and the layer-0 beam on exact fp32 distances (L2, or 1 - <q,x>),
+                           result = the first k of W; n_coarse bounds the traced C, n_rerank /
+                           early_term / assemble_mode are ignored.  GATHER kernels only (an INLINE
+                           index is searched through its GATHER arrays). */
 } aqr_search_params;
+
+enum { AQR_TRAVERSAL_AQR = 0, AQR_TRAVERSAL_FP32 = 1 };
 
 #define AQR_NCOUNT 15
 /* counter slots: 0 expansions, 1 layer-0 degree sum, 2 layer-0 code evaluations, 3 upper

@@ -59,7 +59,7 @@ class _Index(C.Structure):
 class _Params(C.Structure):
     _fields_ = [("k", C.c_int32), ("ef", C.c_int32), ("n_coarse", C.c_int32), ("n_rerank", C.c_int32),
                 ("tau_gap", C.c_double), ("tau_ratio", C.c_double), ("early_term", C.c_int32),
-                ("assemble_mode", C.c_int32), ("beam_form", C.c_int32)]
+                ("assemble_mode", C.c_int32), ("beam_form", C.c_int32), ("traversal", C.c_int32)]
 
 
 def _c(a, dt):
@@ -155,8 +155,9 @@ class Index:
         self.s = s
 
 
-def _params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, beam_form):
+def _params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, beam_form, traversal=0):
     p = _Params()
+    p.traversal = {"aqr": 0, "fp32": 1}[traversal] if isinstance(traversal, str) else int(traversal)
     p.k, p.ef, p.n_coarse, p.n_rerank = k, ef, n_coarse, n_rerank
     p.tau_gap, p.tau_ratio = tau_gap, tau_ratio
     p.early_term, p.assemble_mode, p.beam_form = int(early_term), assemble_mode, beam_form
@@ -164,12 +165,15 @@ def _params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_
 
 
 def search(ix: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True,
-           assemble_mode=0, beam_form=0, trace=False, exp_cap=4096):
+           assemble_mode=0, beam_form=0, trace=False, exp_cap=4096, traversal="aqr"):
+    """traversal="aqr": Alg2.  traversal="fp32": the paper's baseline HNSW search
+     on the same graph -- greedy + flag-form beam on exact fp32 distances in the canonical
+    order R(L) (R22), result = the first k of W; coarse_dq then holds fp32 bits."""
     q = _c(q, np.float32)
     nq = q.shape[0]
     ids = np.zeros((nq, k), np.int32)
     dist = np.zeros((nq, k), np.float32)
-    p = _params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, beam_form)
+    p = _params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, beam_form, traversal)
     tr = {}
     if trace:
         tr = dict(exp_ids=np.full((nq, exp_cap), -1, np.int32),
@@ -263,6 +267,15 @@ def dist_asym(q, xc, min_f, scale_f, metric="l2"):
     q, xc = _c(q, np.float32), _c(xc, np.uint8)
     mn, sc = _c(min_f, np.float32), _c(scale_f, np.float32)
     return float(L.or_dist_asym(_p(q), _p(xc), _p(mn), _p(sc), C.c_int32(len(q)), C.c_int32(0 if metric == "l2" else 1)))
+
+
+def dist_fp_RL(q, x, metric="l2"):
+    """Exact fp32 distance in the canonical order R(L) of the FP32-HNSW baseline (R22)."""
+    L = lib()
+    L.or_dist_fp_RL.restype = C.c_float
+    q = _c(q, np.float32)
+    x = _c(x, np.float32)
+    return float(L.or_dist_fp_RL(_p(q), _p(x), C.c_int32(len(q)), C.c_int32(0 if metric == "l2" else 1)))
 
 
 def dist_exact(q, x, metric="l2"):

@@ -208,6 +208,7 @@ typedef struct {
   double tau_gap, tau_ratio;
   int32_t early_term, assemble_mode; /* 0 = fill (R10), 1 = union */
   int32_t beam_form;                 /* 0 = flag form (R8), 1 = Malkov heap form */
+  int32_t traversal;                 /* 0 = AQR (Alg2), 1 = FP32-HNSW baseline */
 } or_params;
 
 /* per-query trace; any pointer may be NULL */
@@ -500,6 +501,130 @@ static int search_one(const or_index *ix, const float *q, const or_params *p, ui
   return rerank_one(ix, q, cids, nc, p, out_ids, out_d, tr);
 }
 
+/* ------------------------------------------------------------------------------------ */
+/* FP32-HNSW baseline (the paper's comparison system "HNSW"):   */
+/* the same greedy descent and layer-0 beam, on exact fp32 distances, result = the first   */
+/* k of W (no quantizer, no re-rank).                                                       */
+/* ------------------------------------------------------------------------------------ */
+
+/* Exact fp32 distance in the canonical order R(L) (R22): the padded
+ * row (d8 = d rounded up to 8) is cut into 8-float chunks; chunk t belongs to partial l = t mod
+ * L; partial l accumulates its chunks in increasing t, elements in increasing j, one FMA per
+ * element; then for off = L/2 .. 1 every partial becomes p[l] + p[l ^ off]; the result
+ * is p[0].  L = the smallest power of two >= the chunk count, capped at 32.  L2: sum (q - x)^2;
+ * inner product: 1 - sum q x (R12). */
+static float fp_dist_RL(const float *q, const float *x, int32_t d, int32_t metric) {
+  int32_t nch = (d + 7) / 8, L = 1;
+  while (L < nch) L *= 2;
+  if (L > 32) L = 32;
+  float p[32], t2[32];
+  for (int32_t l = 0; l < L; ++l) {
+    float acc = 0.0f;
+    for (int32_t t = l; t < nch; t += L) {
+      for (int32_t j = 8 * t; j < 8 * t + 8 && j < d; ++j) {
+        if (metric == 0) {
+          float e = q[j] - x[j];
+          acc = fmaf(e, e, acc);
+        } else {
+          acc = fmaf(q[j], x[j], acc);
+        }
+      }
+    }
+    p[l] = acc;
+  }
+  for (int32_t off = L / 2; off >= 1; off /= 2) {
+    for (int32_t l = 0; l < L; ++l) t2[l] = p[l] + p[l ^ off];
+    for (int32_t l = 0; l < L; ++l) p[l] = t2[l];
+  }
+  return metric == 0 ? p[0] : 1.0f - p[0];
+}
+
+static int fkey_less(float da, int32_t ia, float db, int32_t ib) {
+  return (da < db) || (da == db && ia < ib);
+}
+
+typedef struct { float d; int32_t id; uint8_t expanded; } or_fent;
+
+/* greedy descent + flag-form beam on exact distances (same algorithm as greedy / beam_flag) */
+static int search_one_fp(const or_index *ix, const float *q, const or_params *p, uint8_t *visited,
+                         or_fent *W, int32_t *out_ids, float *out_d, or_trace *tr) {
+  int64_t *cnt = tr ? tr->counters : NULL;
+  int32_t cur = ix->entry_point;
+  float dcur = fp_dist_RL(q, ix->base + (int64_t)cur * ix->d, ix->d, ix->metric);
+  if (cnt) cnt[C_UPPER_EVALS] += 1;
+  for (int32_t L = ix->max_level; L >= 1; --L) {
+    for (;;) {
+      int32_t cap;
+      const int32_t *row = nbr_row(ix, cur, L, &cap);
+      int32_t best = cur, deg = 0;
+      float dbest = dcur;
+      for (int32_t t = 0; t < cap; ++t) {
+        int32_t u = row[t];
+        if (u < 0) continue;
+        ++deg;
+        float du = fp_dist_RL(q, ix->base + (int64_t)u * ix->d, ix->d, ix->metric);
+        if (cnt) cnt[C_UPPER_EVALS] += 1;
+        if (fkey_less(du, u, dbest, best)) { best = u; dbest = du; }
+      }
+      if (cnt) { cnt[C_UPPER_EXP] += 1; cnt[C_UPPER_DEG_SUM] += deg; }
+      if (best == cur) break;
+      cur = best;
+      dcur = dbest;
+    }
+  }
+  memset(visited, 0, (size_t)ix->n);
+  int32_t size = 1, ef = p->ef, nexp = 0;
+  W[0].d = dcur; W[0].id = cur; W[0].expanded = 0;
+  visited[cur] = 1;
+  for (;;) {
+    int32_t ci = -1;
+    for (int32_t i = 0; i < size; ++i)
+      if (!W[i].expanded) { ci = i; break; }
+    if (ci < 0) break;
+    W[ci].expanded = 1;
+    int32_t c = W[ci].id;
+    if (tr && tr->exp_ids && nexp < tr->exp_cap) tr->exp_ids[nexp] = c;
+    ++nexp;
+    int32_t cap;
+    const int32_t *row = nbr_row(ix, c, 0, &cap);
+    int32_t deg = 0;
+    for (int32_t t = 0; t < cap; ++t) {
+      int32_t u = row[t];
+      if (u < 0) continue;
+      ++deg;
+      if (visited[u]) continue;
+      visited[u] = 1;
+      float du = fp_dist_RL(q, ix->base + (int64_t)u * ix->d, ix->d, ix->metric);
+      if (cnt) cnt[C_EVALS] += 1;
+      if (size < ef || fkey_less(du, u, W[size - 1].d, W[size - 1].id)) {
+        int32_t pos = size < ef ? size : ef - 1;
+        while (pos > 0 && fkey_less(du, u, W[pos - 1].d, W[pos - 1].id)) {
+          W[pos] = W[pos - 1];
+          --pos;
+        }
+        W[pos].d = du; W[pos].id = u; W[pos].expanded = 0;
+        if (size < ef) ++size;
+      }
+    }
+    if (cnt) cnt[C_DEG_SUM] += deg;
+  }
+  if (cnt) { cnt[C_EXPANSIONS] += nexp; cnt[C_NC] = size < p->n_coarse ? size : p->n_coarse; }
+  int32_t nc = p->n_coarse < size ? p->n_coarse : size;
+  for (int32_t i = 0; i < nc; ++i) {
+    if (tr && tr->coarse_ids) tr->coarse_ids[i] = W[i].id;
+    if (tr && tr->coarse_dq) memcpy(&tr->coarse_dq[i], &W[i].d, sizeof(float));  /* the fp32 bits */
+  }
+  for (int32_t i = 0; i < p->k; ++i) {
+    if (i < size) { out_ids[i] = W[i].id; out_d[i] = W[i].d; }
+    else { out_ids[i] = -1; out_d[i] = INFINITY; }
+  }
+  return OR_OK;
+}
+
+float or_dist_fp_RL(const float *q, const float *x, int32_t d, int32_t metric) {
+  return fp_dist_RL(q, x, d, metric);
+}
+
 static int check_params(const or_params *p) {
   if (p->k < 1 || p->n_coarse < p->k || p->ef < p->n_coarse || p->n_rerank < 0 ||
       p->n_rerank > p->n_coarse || p->tau_gap < 0 || p->tau_ratio < 1)
@@ -518,8 +643,12 @@ int or_search(const or_index *ix, const float *q, int64_t nq, const or_params *p
   uint8_t *qc = (uint8_t *)calloc((size_t)ix->d_pad, 1);
   uint8_t *visited = (uint8_t *)malloc((size_t)ix->n);
   or_went *W = (or_went *)malloc(sizeof(or_went) * (size_t)(p->ef + 1));
+  or_fent *WF = (or_fent *)malloc(sizeof(or_fent) * (size_t)(p->ef + 1));
   int32_t *cids = (int32_t *)malloc(sizeof(int32_t) * (size_t)(p->n_coarse + 1));
-  if (!qc || !visited || !W || !cids) { free(qc); free(visited); free(W); free(cids); return OR_ENOMEM; }
+  if (!qc || !visited || !W || !WF || !cids) {
+    free(qc); free(visited); free(W); free(WF); free(cids);
+    return OR_ENOMEM;
+  }
   int st = OR_OK;
   for (int64_t i = 0; i < nq && st == OR_OK; ++i) {
     or_trace tr;
@@ -533,10 +662,13 @@ int or_search(const or_index *ix, const float *q, int64_t nq, const or_params *p
     tr.exact_d = exact_d ? exact_d + i * nc : NULL;
     tr.counters = counters ? counters + i * OR_NCOUNT : NULL;
     if (tr.counters) memset(tr.counters, 0, sizeof(int64_t) * OR_NCOUNT);
-    st = search_one(ix, q + i * ix->d, p, qc, visited, W, cids, out_ids + i * p->k,
-                    out_d + i * p->k, &tr);
+    if (p->traversal == 1)
+      st = search_one_fp(ix, q + i * ix->d, p, visited, WF, out_ids + i * p->k, out_d + i * p->k, &tr);
+    else
+      st = search_one(ix, q + i * ix->d, p, qc, visited, W, cids, out_ids + i * p->k,
+                      out_d + i * p->k, &tr);
   }
-  free(qc); free(visited); free(W); free(cids);
+  free(qc); free(visited); free(W); free(WF); free(cids);
   return st;
 }
 

@@ -49,7 +49,8 @@ class IndexDesc(C.Structure):
 class SearchParams(C.Structure):
     _fields_ = [("k", C.c_int32), ("ef", C.c_int32), ("n_coarse", C.c_int32), ("n_rerank", C.c_int32),
                 ("tau_gap", C.c_double), ("tau_ratio", C.c_double), ("early_term", C.c_int32),
-                ("assemble_mode", C.c_int32), ("visited_bits", C.c_int32), ("warps_per_block", C.c_int32)]
+                ("assemble_mode", C.c_int32), ("visited_bits", C.c_int32), ("warps_per_block", C.c_int32),
+                ("traversal", C.c_int32)]
 
 
 class Debug(C.Structure):
@@ -247,9 +248,13 @@ def ef_mapping(ef: int, k: int, m_ef: int = 3, n_rerank_preset: int = 28):
     return dict(ef=max(ef, n_c), n_coarse=n_c, n_rerank=min(max(k, n_rerank_preset), n_c))
 
 
+TRAVERSALS = {"aqr": 0, "fp32": 1}
+
+
 def make_params(k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True, assemble_mode=0,
-                visited_bits=0, warps_per_block=0) -> SearchParams:
+                visited_bits=0, warps_per_block=0, traversal="aqr") -> SearchParams:
     p = SearchParams()
+    p.traversal = TRAVERSALS[traversal]
     p.k, p.ef, p.n_coarse, p.n_rerank = k, ef, n_coarse, n_rerank
     p.tau_gap, p.tau_ratio = tau_gap, tau_ratio
     p.early_term, p.assemble_mode = int(bool(early_term)), assemble_mode
@@ -283,13 +288,14 @@ class Searcher:
 
 
 def search(index: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True,
-           assemble_mode=0, visited_bits=0, warps_per_block=0, trace=False, exp_cap=4096, stream=None):
+           assemble_mode=0, visited_bits=0, warps_per_block=0, trace=False, exp_cap=4096, stream=None,
+           traversal="aqr"):
     """aqr_search on q [nq, d] fp32 CUDA -> (ids [nq, k] int32, dist [nq, k] fp32[, trace dict])."""
     torch = _torch()
     pq = _dev(q, torch.float32, "q")
     nq = q.shape[0]
     p = make_params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, visited_bits,
-                    warps_per_block)
+                    warps_per_block, traversal)
     dev = q.device
     ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
     dist = torch.empty((nq, k), dtype=torch.float32, device=dev)

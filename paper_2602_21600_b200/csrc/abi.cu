@@ -154,7 +154,7 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   V.n = n;
   V.d = D.d;
   V.d_pad = round_up(D.d, 32);  // internal code stride: whole 32-byte chunks (one LDG.256 each)
-  V.d4 = round_up(D.d, 4);
+  V.d4 = round_up(D.d, 8);  // fp32 row stride: whole 32-byte chunks (FP32 traversal loads 8 floats)
   V.metric = (int32_t)D.metric;
   V.id_base = D.id_base;
   V.M = M;
@@ -266,6 +266,8 @@ static aqr_status check_search_params(const aqr_search_params* p, bool need_ef) 
   AQR_CHECK_ARG(p->visited_bits == 0 || p->visited_bits == -1 || (p->visited_bits >= 6 && p->visited_bits <= 16),
                 "search: visited_bits must be 0 (auto), -1 (no visited hash) or in [6, 16]");
   AQR_CHECK_ARG(p->warps_per_block >= 0 && p->warps_per_block <= 8, "search: warps_per_block must be in [0, 8]");
+  AQR_CHECK_ARG(p->traversal == AQR_TRAVERSAL_AQR || p->traversal == AQR_TRAVERSAL_FP32,
+                "search: traversal must be AQR_TRAVERSAL_AQR (0) or AQR_TRAVERSAL_FP32 (1)");
   return AQR_OK;
 }
 
@@ -280,6 +282,7 @@ static aqr::SearchCfg make_cfg(const aqr_search_params* p) {
   c.early_term = p->early_term;
   c.assemble_mode = p->assemble_mode;
   c.hbits = p->visited_bits > 0 ? p->visited_bits : 0;
+  c.fp32 = p->traversal == AQR_TRAVERSAL_FP32;
   return c;
 }
 

@@ -36,6 +36,7 @@ struct SearchCfg {
   double tau_gap, tau_ratio;
   int32_t early_term, assemble_mode;
   int32_t hbits;          // visited hash slots = 1 << hbits
+  int32_t fp32;           // 1: FP32 baseline traversal (exact distances, no quantizer / re-rank)
 };
 
 void set_error(const std::string& msg);

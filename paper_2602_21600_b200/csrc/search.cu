@@ -322,6 +322,85 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg
 }
 
 // ------------------------------------------------------------------------------------
+// FP32 baseline traversal (AQR_TRAVERSAL_FP32): exact distances of the query (fp32, shared
+// memory) to a list of base rows (fp32, d4 = round_up(d, 8) floats).  LPR lanes per row, lane
+// `sub` owns the 32-byte chunks c = sub + LPR t (one LDG.256 each); canonical order R(LPR):
+// each lane accumulates its chunks in increasing c with one FMA per element, then a butterfly
+// over the LPR lanes (offsets LPR/2 .. 1).  The key written is the order-preserving uint32 of
+// the distance (fkey), so W and its (key, id) order are shared with the quantized path.
+// ------------------------------------------------------------------------------------
+template <int LPR>
+__device__ __forceinline__ void fp_dists(const IndexView& ix, const float* qf, const int32_t* ids, int m,
+                                         int32_t* out, int lane) {
+  constexpr int G = 32 / LPR;
+  constexpr int U = 4;  // rows per lane per pass (32 B each; half the AQR pass: the query chunk and
+                        // the fp32 partial sums need the registers); nb is padded for 8
+  const int g = lane / LPR, sub = lane % LPR;
+  const int nchf = ix.d4 >> 3;
+  for (int r0 = 0; r0 < m; r0 += G * U) {
+    int idv[U];
+#pragma unroll
+    for (int u4 = 0; u4 < U; u4 += 4) {
+      const int4 t4 = *reinterpret_cast<const int4*>(ids + r0 + g * U + u4);
+      idv[u4] = t4.x;
+      idv[u4 + 1] = t4.y;
+      idv[u4 + 2] = t4.z;
+      idv[u4 + 3] = t4.w;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (r0 + g * U + u >= m) idv[u] = -1;
+    float part[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) part[u] = 0.0f;
+    for (int c = sub; c < nchf; c += LPR) {
+      C32 buf[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (idv[u] >= 0) {
+          ldg256(ix.base + (int64_t)idv[u] * ix.d4 + 8 * c, buf[u]);
+        } else {
+          buf[u].a = make_uint4(0, 0, 0, 0);
+          buf[u].b = make_uint4(0, 0, 0, 0);
+        }
+      }
+      const float4 qa = reinterpret_cast<const float4*>(qf)[2 * c];
+      const float4 qb = reinterpret_cast<const float4*>(qf)[2 * c + 1];
+      const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t xw[8] = {buf[u].a.x, buf[u].a.y, buf[u].a.z, buf[u].a.w,
+                                buf[u].b.x, buf[u].b.y, buf[u].b.z, buf[u].b.w};
+        float acc = part[u];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float xv = __uint_as_float(xw[e]);
+          if (ix.metric == 0) {
+            const float df = __fsub_rn(qv[e], xv);
+            acc = __fmaf_rn(df, df, acc);
+          } else {
+            acc = __fmaf_rn(qv[e], xv, acc);
+          }
+        }
+        part[u] = acc;
+      }
+    }
+#pragma unroll
+    for (int off = LPR / 2; off >= 1; off >>= 1) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) part[u] = __fadd_rn(part[u], __shfl_xor_sync(kFull, part[u], off));
+    }
+    if (sub == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = r0 + g * U + u;
+        if (r < m) out[r] = (int32_t)fkey(ix.metric == 0 ? part[u] : __fsub_rn(1.0f, part[u]));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // visited set: open-addressing hash of node ids in shared memory.  A full probe window
 // reports "not visited" and overwrites the window's last slot (so the table keeps the most
 // recently seen ids): a false negative only causes a re-evaluation, which the W dedupe
@@ -579,7 +658,7 @@ __device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, c
 // next block prefetched during the merge) or the GATHER layout (row + per-code gathers,
 // shared-memory visited hash)
 // ------------------------------------------------------------------------------------
-template <int LPR, int CPL, bool INL, int CAP>
+template <int LPR, int CPL, bool INL, int CAP, bool FP>
 __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_kernel(IndexView ix, SearchCfg c, Layout L, const float* __restrict__ q,
                                                      int64_t nq, int64_t ld_q, int32_t* __restrict__ out_ids,
                                                      float* __restrict__ out_dist, aqr_debug dbg, int has_dbg,
@@ -623,24 +702,31 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     int fails = 0;
 
     // 1. quantize the query
-    load_query(ix, q, ld_q, qi, qf, qc, lane);
+    load_query(ix, q, ld_q, qi, qf, FP ? nullptr : qc, lane);
     C32 qreg[CPL];
-#pragma unroll
-    for (int t = 0; t < CPL; ++t) {
-      const int ch = sub + LPR * t;
-      qreg[t].a = ch < nch ? reinterpret_cast<const uint4*>(qc)[2 * ch] : make_uint4(0, 0, 0, 0);
-      qreg[t].b = ch < nch ? reinterpret_cast<const uint4*>(qc)[2 * ch + 1] : make_uint4(0, 0, 0, 0);
-    }
     int qq = 0;
-    for (int j = lane; j < ix.d_pad; j += 32) qq += (int)qc[j] * (int)qc[j];
+    if (!FP) {
 #pragma unroll
-    for (int off = 16; off; off >>= 1) qq += __shfl_xor_sync(kFull, qq, off);
+      for (int t = 0; t < CPL; ++t) {
+        const int ch = sub + LPR * t;
+        qreg[t].a = ch < nch ? reinterpret_cast<const uint4*>(qc)[2 * ch] : make_uint4(0, 0, 0, 0);
+        qreg[t].b = ch < nch ? reinterpret_cast<const uint4*>(qc)[2 * ch + 1] : make_uint4(0, 0, 0, 0);
+      }
+      for (int j = lane; j < ix.d_pad; j += 32) qq += (int)qc[j] * (int)qc[j];
+#pragma unroll
+      for (int off = 16; off; off >>= 1) qq += __shfl_xor_sync(kFull, qq, off);
+    }
+    // distance keys of a list of node ids: d^q (the method) or the fp32 baseline's exact distance
+    auto dists = [&](const int32_t* ids_, int m_, int32_t* out_) {
+      if (FP) fp_dists<LPR>(ix, qf, ids_, m_, out_, lane);
+      else list_dists<LPR, CPL>(ix, qreg, qq, ids_, m_, out_, lane);
+    };
 
     // 2. greedy descent through the upper layers (R8)
     int32_t cur = ix.entry;
     if (lane == 0) nb[0] = cur;
     __syncwarp();
-    list_dists<LPR, CPL>(ix, qreg, qq, nb, 1, nd, lane);
+    dists(nb, 1, nd);
     __syncwarp();
     uint32_t dcur = (uint32_t)nd[0];
     cnt[5] += 1;
@@ -650,7 +736,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         const int32_t* row = ix.adj_up + (int64_t)(__ldg(ix.up_off + cur) + lv - 1) * ix.M;
         int deg;
         const int m = gather_row(row, ix.M, nb, nullptr, 0, fails, deg, lane);
-        list_dists<LPR, CPL>(ix, qreg, qq, nb, m, nd, lane);
+        dists(nb, m, nd);
         __syncwarp();
         uint64_t best = qkey(dcur, cur);
         for (int r = lane; r < m; r += 32) {
@@ -765,7 +851,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         ids = nb;
         cnt[1] += deg;
         cnt[2] += m;
-        list_dists<LPR, CPL>(ix, qreg, qq, nb, m, nd, lane);
+        dists(nb, m, nd);
       }
       __syncwarp();
       // filter against max W (when full), then drop re-evaluations already in W (R15): the
@@ -901,8 +987,32 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       for (int i = lane; i < c.n_coarse; i += 32) {
         const uint64_t wkk = i < nc ? W[i] : 0;
         if (dbg.coarse_ids) dbg.coarse_ids[qi * c.n_coarse + i] = i < nc ? qkey_id(wkk) : -1;
-        if (dbg.coarse_dq) dbg.coarse_dq[qi * c.n_coarse + i] = i < nc ? (int32_t)qkey_d(wkk) : -1;
+        if (dbg.coarse_dq)
+          dbg.coarse_dq[qi * c.n_coarse + i] =
+              i < nc ? (FP ? __float_as_int(fkey_inv(qkey_d(wkk))) : (int32_t)qkey_d(wkk)) : -1;
       }
+    }
+    if (FP) {
+      // the baseline's result: the first k entries of W, distances exact already
+      for (int t = lane; t < c.k; t += 32) {
+        int32_t oid = -1;
+        float od = INFINITY;
+        if (t < size) {
+          oid = (int32_t)((int64_t)qkey_id(W[t]) + ix.id_base);
+          od = fkey_inv(qkey_d(W[t]));
+        }
+        out_ids[qi * c.k + t] = oid;
+        out_dist[qi * c.k + t] = od;
+      }
+      if (has_dbg && lane == 0) {
+        if (dbg.counters)
+          for (int t = 0; t < AQR_NCOUNT; ++t) dbg.counters[qi * AQR_NCOUNT + t] = cnt[t];
+        if (dbg.totals)
+          for (int t = 0; t < AQR_NCOUNT; ++t)
+            atomicAdd(reinterpret_cast<unsigned long long*>(dbg.totals + t), (unsigned long long)cnt[t]);
+      }
+      __syncwarp();
+      continue;
     }
     // Stage 2/3 scratch lives in W: unsorted keys overwrite W[0:nc] in place, A goes to
     // W[nc:2nc] (ef >= 2 N_c, as with m_ef >= 2), else to a separate area
@@ -987,13 +1097,13 @@ __global__ void __launch_bounds__(128) rerank_kernel(IndexView ix, SearchCfg c, 
   finish_query(ix, cc, qf, cid, nullptr, nc, akeys, rkeys, qi, out_ids, out_dist, none, false, lane, nullptr);
 }
 
-template <int LPR, int CPL, bool INL, int CAP>
+template <int LPR, int CPL, bool INL, int CAP, bool FP = false>
 cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                      int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
                      cudaStream_t s) {
   const Layout L = make_layout(ix, c, Hot<LPR, CPL, CAP>::bytes);
   const size_t smem = (size_t)L.per_warp * wpb;
-  auto kern = search_kernel<LPR, CPL, INL, CAP>;
+  auto kern = search_kernel<LPR, CPL, INL, CAP, FP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
@@ -1017,8 +1127,14 @@ cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, in
 struct Shape {
   int lpr, cpl, cap;
 };
-Shape shape_of(const IndexView& ix) {
-  const int nch = ix.d_pad >> 5;
+Shape shape_of(const IndexView& ix, bool fp = false) {
+  const int nch = fp ? (ix.d4 >> 3) : (ix.d_pad >> 5);  // 32-byte chunks of a code / fp32 row
+  if (fp) {
+    int lpr = 1;
+    while (lpr < nch) lpr <<= 1;
+    if (lpr > 32) lpr = 32;
+    return Shape{lpr, 1, ix.cap0 <= 64 ? 64 : 160};
+  }
   int lpr = 1;
   while (lpr < nch) lpr <<= 1;
   if (lpr > 32) lpr = 32;
@@ -1038,9 +1154,9 @@ Shape shape_of(const IndexView& ix) {
     default: break;                                                                \
   }
 
-int hot_bytes(const IndexView& ix) {
+int hot_bytes(const IndexView& ix, bool fp) {
 #define AQR_HOT(L_, C_, K_) return Hot<L_, C_, K_>::bytes
-  AQR_DISPATCH(shape_of(ix), AQR_HOT)
+  AQR_DISPATCH(shape_of(ix, fp), AQR_HOT)
 #undef AQR_HOT
   return -1;
 }
@@ -1048,7 +1164,7 @@ int hot_bytes(const IndexView& ix) {
 }  // namespace
 
 size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int wpb) {
-  const int hb = hot_bytes(ix);
+  const int hb = hot_bytes(ix, c.fp32 != 0);
   if (hb < 0) return ~(size_t)0;
   return (size_t)make_layout(ix, c, hb).per_warp * wpb;
 }
@@ -1056,6 +1172,22 @@ size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int wpb) {
 cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                           int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
                           cudaStream_t s) {
+  if (c.fp32) {
+    // the baseline runs the GATHER kernel (an INLINE index keeps its GATHER arrays)
+#define AQR_LAUNCH_FP(L_, C_, K_) \
+  return launch_t<L_, 1, false, K_, true>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)
+    const Shape sh = shape_of(ix, true);
+    switch (sh.lpr * 1000 + sh.cap) {
+      case 1064: AQR_LAUNCH_FP(1, 1, 64); case 1160: AQR_LAUNCH_FP(1, 1, 160);
+      case 2064: AQR_LAUNCH_FP(2, 1, 64); case 2160: AQR_LAUNCH_FP(2, 1, 160);
+      case 4064: AQR_LAUNCH_FP(4, 1, 64); case 4160: AQR_LAUNCH_FP(4, 1, 160);
+      case 8064: AQR_LAUNCH_FP(8, 1, 64); case 8160: AQR_LAUNCH_FP(8, 1, 160);
+      case 16064: AQR_LAUNCH_FP(16, 1, 64); case 16160: AQR_LAUNCH_FP(16, 1, 160);
+      case 32064: AQR_LAUNCH_FP(32, 1, 64); case 32160: AQR_LAUNCH_FP(32, 1, 160);
+      default: return cudaErrorInvalidValue;
+    }
+#undef AQR_LAUNCH_FP
+  }
   const bool inl = ix.blk != nullptr;
 #define AQR_LAUNCH(L_, C_, K_)                                                                            \
   return inl ? launch_t<L_, C_, true, K_>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)    \
