@@ -74,13 +74,12 @@ __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
   uint32_t lo = __shfl_sync(kFull, (uint32_t)v, src), hi = __shfl_sync(kFull, (uint32_t)(v >> 32), src);
   return ((uint64_t)hi << 32) | lo;
 }
+// warp-wide 64-bit minimum: two redux.sync (REDUX) on the high then the low word
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
-#pragma unroll
-  for (int m = 16; m; m >>= 1) {
-    uint64_t o = shfl_xor_u64(v, m);
-    v = o < v ? o : v;
-  }
-  return v;
+  const uint32_t hi = (uint32_t)(v >> 32);
+  const uint32_t mh = __reduce_min_sync(kFull, hi);
+  const uint32_t ml = __reduce_min_sync(kFull, hi == mh ? (uint32_t)v : 0xffffffffu);
+  return ((uint64_t)mh << 32) | ml;
 }
 
 // ---- mbarrier + bulk (TMA) copy helpers (sm_90+ PTX; UBLKCP in SASS) ----
