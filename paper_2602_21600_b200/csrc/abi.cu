@@ -283,6 +283,7 @@ static aqr::SearchCfg make_cfg(const aqr_search_params* p) {
   c.assemble_mode = p->assemble_mode;
   c.hbits = p->visited_bits > 0 ? p->visited_bits : 0;
   c.fp32 = p->traversal == AQR_TRAVERSAL_FP32;
+  c.staged = 0;  // chosen per launch by launch_search
   return c;
 }
 

@@ -37,6 +37,7 @@ struct SearchCfg {
   int32_t early_term, assemble_mode;
   int32_t hbits;          // visited hash slots = 1 << hbits
   int32_t fp32;           // 1: FP32 baseline traversal (exact distances, no quantizer / re-rank)
+  int32_t staged;         // set by the launcher: wide code rows gathered through a TMA stage
 };
 
 void set_error(const std::string& msg);

@@ -123,6 +123,8 @@ __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t 
 // ------------------------------------------------------------------------------------
 // per-warp shared-memory layout
 // ------------------------------------------------------------------------------------
+constexpr int kStage = 8;  // rows per stage buffer of the staged (TMA) wide-row gather
+
 struct Layout {
   // runtime part of the per-warp layout; the hot arrays of the beam (Hot<> below) sit at
   // compile-time offsets before W, so every access to them is [warp base + immediate]
@@ -162,6 +164,10 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   L.o_qf = o; o += al16(4 * ix.d4);
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
   L.region = ix.blk ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
+  if (c.staged) {  // staged_dists: 2 x kStage wide rows
+    const int st = 2 * kStage * ix.d_pad;
+    if (st > L.region) L.region = st;
+  }
   o = (o + 127) & ~127;
   L.o_h = o; o += al16(L.region);
   L.o_s23 = o; o += c.ef >= 2 * c.n_coarse ? 0 : al16(8 * c.n_coarse);
@@ -317,6 +323,77 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg
 #pragma unroll
     for (int v = 0; v < PER; ++v) part[v] += xn[v];
     store_rows<LPR, U>(part, r0, g, sub, m, qq, out);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// d^q for wide code rows (d_pad > 512, LPR = 32: one row per warp step, e.g. C4 d = 960): a
+// register pass holds only U = 8 rows, so a 140-neighbour expansion would take ~18 dependent
+// round trips.  Instead the rows are bulk-copied (cp.async.bulk, TMA) into a double-buffered
+// shared stage of kStage rows each, the copies of chunk i+1 in flight while chunk i is scored:
+// about one round trip per expansion.  Same arithmetic as list_dists (exact int32 d^q).
+// ------------------------------------------------------------------------------------
+template <int CPL>
+__device__ __forceinline__ void staged_dists(const IndexView& ix, const C32 (&qreg)[CPL], int qq, const int32_t* ids,
+                                             int m, int32_t* out, int lane, uint8_t* stage, uint64_t* bars,
+                                             uint32_t& ph) {
+  constexpr int LPR = 32, U = kStage;
+  const int nch = ix.d_pad >> 5;
+  const int nck = (m + U - 1) / U;
+  auto issue = [&](int ck) {
+    const int b = ck & 1, r0 = ck * U;
+    const int id = (lane < U && r0 + lane < m) ? ids[r0 + lane] : -1;
+    const int nv = __popc(__ballot_sync(kFull, id >= 0));
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async();
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bars + b)),
+                   "r"((uint32_t)(nv * ix.d_pad))
+                   : "memory");
+    }
+    __syncwarp();
+    if (id >= 0) {
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(stage + (size_t)(b * U + lane) * ix.d_pad)),
+          "l"(ix.codes + (int64_t)id * ix.d_pad), "r"((uint32_t)ix.d_pad), "r"(smem_u32(bars + b))
+          : "memory");
+    }
+  };
+  if (nck > 0) issue(0);
+  for (int ck = 0; ck < nck; ++ck) {
+    if (ck + 1 < nck) issue(ck + 1);
+    const int b = ck & 1, r0 = ck * U;
+    // |x^|^2 of the row this lane will hold (REP = LPR / U lanes per row)
+    constexpr int REP = LPR / U;
+    const int ur = lane / REP;
+    const int idr = r0 + ur < m ? ids[r0 + ur] : -1;
+    const int xn = idr >= 0 ? __ldg(ix.xnorm + idr) : 0;
+    mbar_wait(bars + b, (ph >> b) & 1u);
+    ph ^= 1u << b;
+    int part[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      unsigned qx = 0;
+      const int r = r0 + u;
+      const uint4* row = reinterpret_cast<const uint4*>(stage + (size_t)(b * U + u) * ix.d_pad);
+      if (r < m && ids[r] >= 0) {
+#pragma unroll
+        for (int t = 0; t < CPL; ++t) {
+          const int c = lane + LPR * t;
+          if (c < nch) {
+            C32 w;
+            w.a = row[2 * c];
+            w.b = row[2 * c + 1];
+            dp4a_qx(w, qreg[t], qx);
+          }
+        }
+      }
+      part[u] = -2 * (int)qx;
+    }
+    reduce_rows<LPR, U>(part, lane);
+    if ((lane % REP) == 0 && r0 + ur < m) out[r0 + ur] = qq + part[0] + xn;
+    __syncwarp();  // the stage buffer is read before it is refilled
   }
 }
 
@@ -682,9 +759,13 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
   const int nch = ix.d_pad >> 5;
   const int ef = c.ef;
   uint32_t phase = 0u;
-  if (INL) {
+  // wide rows: staged (TMA) gather, when the launcher chose it (c.staged)
+  const bool STG = !INL && !FP && LPR == 32 && c.staged;
+  uint32_t sph = 0u;                               // staged_dists parities (bit per buffer)
+  if (INL || STG) {
     if (lane == 0) {
       mbar_init(bar, 1);
+      if (STG) mbar_init(bar + 1, 1);
       fence_proxy_async();
     }
     __syncwarp();
@@ -718,6 +799,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     // distance keys of a list of node ids: d^q (the method) or the fp32 baseline's exact distance
     auto dists = [&](const int32_t* ids_, int m_, int32_t* out_) {
       if (FP) fp_dists<LPR>(ix, qf, ids_, m_, out_, lane);
+      else if (LPR == 32 && STG) staged_dists<CPL>(ix, qreg, qq, ids_, m_, out_, lane, blkbuf, bar, sph);
       else list_dists<LPR, CPL>(ix, qreg, qq, ids_, m_, out_, lane);
     };
 
@@ -1100,24 +1182,53 @@ template <int LPR, int CPL, bool INL, int CAP, bool FP = false>
 cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                      int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
                      cudaStream_t s) {
-  const Layout L = make_layout(ix, c, Hot<LPR, CPL, CAP>::bytes);
-  const size_t smem = (size_t)L.per_warp * wpb;
   auto kern = search_kernel<LPR, CPL, INL, CAP, FP>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int dev = 0, nsm = 0, per_sm = 0;
+  int dev = 0, nsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem);
+  // resident warps for a configuration (per-warp shared memory at CTA size w)
+  auto resident = [&](const Layout& Lx, int w, int* per_sm_out) -> cudaError_t {
+    const size_t sm = (size_t)Lx.per_warp * w;
+    cudaError_t er = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (er != cudaSuccess) return er;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm_out, kern, w * 32, sm);
+  };
+  SearchCfg cc = c;
+  cc.staged = 0;
+  Layout L = make_layout(ix, cc, Hot<LPR, CPL, CAP>::bytes);
+  if (L.per_warp > 12 * 1024) wpb = 1;  // large per-warp state: pack the SMs warp by warp
+  int per_sm = 0;
+  cudaError_t e = resident(L, wpb, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (!INL && !FP && LPR == 32) {
+    // wide code rows: stage them by TMA unless the stage costs concurrently running queries
+    SearchCfg cs = c;
+    cs.staged = 1;
+    const Layout Ls = make_layout(ix, cs, Hot<LPR, CPL, CAP>::bytes);
+    const int ws = Ls.per_warp > 12 * 1024 ? 1 : wpb;
+    int per_sm_s = 0;
+    e = resident(Ls, ws, &per_sm_s);
+    if (e != cudaSuccess) return e;
+    const int64_t run0 = (int64_t)nsm * per_sm * wpb, run1 = (int64_t)nsm * per_sm_s * ws;
+    const int64_t need = nq < run0 ? nq : run0;
+    if (per_sm_s >= 1 && run1 >= need) {
+      cc = cs;
+      L = Ls;
+      wpb = ws;
+      per_sm = per_sm_s;
+    }
+  }
+  e = resident(L, wpb, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const size_t smem = (size_t)L.per_warp * wpb;
   int64_t want = (nq + wpb - 1) / wpb;
   int64_t grid = (int64_t)nsm * per_sm;
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
   aqr_debug d{};
   if (dbg) d = *dbg;
-  kern<<<(unsigned)grid, wpb * 32, smem, s>>>(ix, c, L, q, nq, ld_q, out_ids, out_dist, d, dbg ? 1 : 0, counter);
+  kern<<<(unsigned)grid, wpb * 32, smem, s>>>(ix, cc, L, q, nq, ld_q, out_ids, out_dist, d, dbg ? 1 : 0, counter);
   return cudaGetLastError();
 }
 
