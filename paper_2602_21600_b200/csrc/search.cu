@@ -35,6 +35,9 @@ namespace {
 #ifndef AQR_MIN_CTAS
 #define AQR_MIN_CTAS 6  // 6 CTAs x 4 warps (<= 85 regs): the shared-memory limit at ef ~ 800
 #endif
+#ifndef AQR_SEARCH4
+#define AQR_SEARCH4 0  // 1: 4-ary W lower bound (three probes per step; measured slower at throughput)
+#endif
 #ifndef AQR_ROWS_PER_PASS
 #define AQR_ROWS_PER_PASS 16  // 16-byte code chunks in flight per lane per gather pass
 #endif
@@ -110,14 +113,44 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // number of W keys strictly less than key, ignoring the expanded flag bit
+// (key has flag 0 and keys differ above bit 0, so a[i] < key needs no mask.)  4-ary search: three
+// independent probes per step halve the dependent shared-load chain of a binary search.
 __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t key) {
-  int lo = 0, hi = n;
+#if AQR_SEARCH4
+  int lo = 0, len = n;  // the answer lies in [lo, lo + len]
+  while (len >= 4) {
+    const int p1 = lo + (len >> 2), p2 = lo + (len >> 1), p3 = lo + ((3 * len) >> 2);
+    const uint64_t v1 = a[p1], v2 = a[p2], v3 = a[p3];
+    const int hi = lo + len;
+    if (v3 < key) {
+      lo = p3 + 1;
+      len = hi - lo;
+    } else if (v2 < key) {
+      lo = p2 + 1;
+      len = p3 - lo;
+    } else if (v1 < key) {
+      lo = p1 + 1;
+      len = p2 - lo;
+    } else {
+      len = p1 - lo;
+    }
+  }
+  int hi = lo + len;
   while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (a[mid] < key) lo = mid + 1;  // key has flag 0 and keys differ above bit 0: no mask needed
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1;
     else hi = mid;
   }
   return lo;
+#else
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+#endif
 }
 
 // ------------------------------------------------------------------------------------
