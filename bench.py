@@ -730,7 +730,7 @@ def main():
                     help="aqr: the method; fp32: the paper's baseline HNSW search on the same graph (NEXT-2)")
     ap.add_argument("--rerank", default="auto",
                     help="re-rank depth mappings swept: preset (Table 3, N_rerank = 28) and/or full (N_rerank = N_c); "
-                         "auto = preset for C1/C2 (identical recall there, measured), preset,full for C3/C4")
+                         "auto = preset for C2 (identical recall there, measured), preset,full otherwise")
     ap.add_argument("--vbits", type=lambda v: [int(t) for t in v.split(",")], default=[-1],
                     help="visited-hash sizes (log2 slots, 0 = auto) tried at the chosen ef; fastest is timed")
     ap.add_argument("--threads", type=int, default=0)
@@ -747,7 +747,7 @@ def main():
         log("[bench] warm-up raised to 3 (timing rule)")
         args.warmup = 3
     if args.rerank == "auto":
-        args.rerank = "preset,full" if args.config in ("C3", "C4") else "preset"
+        args.rerank = "preset" if args.config == "C2" else "preset,full"
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "C5":

@@ -162,6 +162,7 @@ struct Layout {
   // runtime part of the per-warp layout; the hot arrays of the beam (Hot<> below) sit at
   // compile-time offsets before W, so every access to them is [warp base + immediate]
   int o_w, o_qc, o_qf, o_h, o_s23, per_warp;
+  int q_alias;    // 1: query codes / fp32 query live in the hot arrays (rebuilt for Stage 2)
   int region;     // bytes of the hash / block-buffer region (reused by Stage 2/3)
   int buf_bytes;  // INLINE: one staged block (128-byte aligned)
 };
@@ -174,7 +175,7 @@ __host__ __device__ constexpr int rows_u() {
   return AQR_ROWS_PER_PASS / (2 * CPL) < 4 ? 4 : AQR_ROWS_PER_PASS / (2 * CPL) / 4 * 4;
 }
 
-// the beam's per-warp scratch for adjacency rows of up to CAP entries (CAP = 64 or 160)
+// the beam's per-warp scratch for adjacency rows of up to CAP entries (CAP = 56 or 160)
 template <int LPR, int CPL, int CAP>
 struct Hot {
   static constexpr int PASS = (32 / LPR) * rows_u<CPL>();  // rows read per list_dists pass
@@ -193,8 +194,16 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   Layout L;
   int o = hot_bytes;
   L.o_w = o; o += al16(8 * (c.ef + 1));
-  L.o_qc = o; o += al16(ix.d_pad);
-  L.o_qf = o; o += al16(4 * ix.d4);
+  // the query (codes + fp32) is only read before the beam and in Stage 2/3: when it fits it
+  // borrows the beam's scratch (AQR traversal; the fp32 baseline reads it throughout)
+  L.q_alias = !c.fp32 && al16(4 * ix.d4) + al16(ix.d_pad) <= hot_bytes;
+  if (L.q_alias) {
+    L.o_qf = 0;
+    L.o_qc = al16(4 * ix.d4);
+  } else {
+    L.o_qc = o; o += al16(ix.d_pad);
+    L.o_qf = o; o += al16(4 * ix.d4);
+  }
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
   L.region = ix.blk ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
   if (c.staged) {  // staged_dists: 2 x kStage wide rows
@@ -1128,6 +1137,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       __syncwarp();
       continue;
     }
+    if (L.q_alias) load_query(ix, q, ld_q, qi, qf, nullptr, lane);  // the beam reused its space
     // Stage 2/3 scratch lives in W: unsorted keys overwrite W[0:nc] in place, A goes to
     // W[nc:2nc] (ef >= 2 N_c, as with m_ef >= 2), else to a separate area
     uint64_t* akeys = ef >= 2 * nc ? W + nc : reinterpret_cast<uint64_t*>(wb + L.o_s23);
@@ -1276,24 +1286,24 @@ Shape shape_of(const IndexView& ix, bool fp = false) {
     int lpr = 1;
     while (lpr < nch) lpr <<= 1;
     if (lpr > 32) lpr = 32;
-    return Shape{lpr, 1, ix.cap0 <= 64 ? 64 : 160};
+    return Shape{lpr, 1, ix.cap0 <= 56 ? 56 : 160};
   }
   int lpr = 1;
   while (lpr < nch) lpr <<= 1;
   if (lpr > 32) lpr = 32;
-  return Shape{lpr, (nch + lpr - 1) / lpr, ix.cap0 <= 64 ? 64 : 160};
+  return Shape{lpr, (nch + lpr - 1) / lpr, ix.cap0 <= 56 ? 56 : 160};
 }
 
 // F(lpr, cpl, cap) dispatch over the instantiated shapes
 #define AQR_DISPATCH(SH, CALL)                                                      \
   switch ((SH).lpr * 1000 + (SH).cpl * 200 + (SH).cap) {                           \
-    case 1264: CALL(1, 1, 64); case 1360: CALL(1, 1, 160);                        \
-    case 2264: CALL(2, 1, 64); case 2360: CALL(2, 1, 160);                        \
-    case 4264: CALL(4, 1, 64); case 4360: CALL(4, 1, 160);                        \
-    case 8264: CALL(8, 1, 64); case 8360: CALL(8, 1, 160);                        \
-    case 16264: CALL(16, 1, 64); case 16360: CALL(16, 1, 160);                    \
-    case 32264: CALL(32, 1, 64); case 32360: CALL(32, 1, 160);                    \
-    case 32464: CALL(32, 2, 64); case 32560: CALL(32, 2, 160);                    \
+    case 1256: CALL(1, 1, 56); case 1360: CALL(1, 1, 160);                        \
+    case 2256: CALL(2, 1, 56); case 2360: CALL(2, 1, 160);                        \
+    case 4256: CALL(4, 1, 56); case 4360: CALL(4, 1, 160);                        \
+    case 8256: CALL(8, 1, 56); case 8360: CALL(8, 1, 160);                        \
+    case 16256: CALL(16, 1, 56); case 16360: CALL(16, 1, 160);                    \
+    case 32256: CALL(32, 1, 56); case 32360: CALL(32, 1, 160);                    \
+    case 32456: CALL(32, 2, 56); case 32560: CALL(32, 2, 160);                    \
     default: break;                                                                \
   }
 
@@ -1321,12 +1331,12 @@ cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* 
   return launch_t<L_, 1, false, K_, true>(ix, c, q, nq, ld_q, out_ids, out_dist, dbg, counter, wpb, s)
     const Shape sh = shape_of(ix, true);
     switch (sh.lpr * 1000 + sh.cap) {
-      case 1064: AQR_LAUNCH_FP(1, 1, 64); case 1160: AQR_LAUNCH_FP(1, 1, 160);
-      case 2064: AQR_LAUNCH_FP(2, 1, 64); case 2160: AQR_LAUNCH_FP(2, 1, 160);
-      case 4064: AQR_LAUNCH_FP(4, 1, 64); case 4160: AQR_LAUNCH_FP(4, 1, 160);
-      case 8064: AQR_LAUNCH_FP(8, 1, 64); case 8160: AQR_LAUNCH_FP(8, 1, 160);
-      case 16064: AQR_LAUNCH_FP(16, 1, 64); case 16160: AQR_LAUNCH_FP(16, 1, 160);
-      case 32064: AQR_LAUNCH_FP(32, 1, 64); case 32160: AQR_LAUNCH_FP(32, 1, 160);
+      case 1056: AQR_LAUNCH_FP(1, 1, 56); case 1160: AQR_LAUNCH_FP(1, 1, 160);
+      case 2056: AQR_LAUNCH_FP(2, 1, 56); case 2160: AQR_LAUNCH_FP(2, 1, 160);
+      case 4056: AQR_LAUNCH_FP(4, 1, 56); case 4160: AQR_LAUNCH_FP(4, 1, 160);
+      case 8056: AQR_LAUNCH_FP(8, 1, 56); case 8160: AQR_LAUNCH_FP(8, 1, 160);
+      case 16056: AQR_LAUNCH_FP(16, 1, 56); case 16160: AQR_LAUNCH_FP(16, 1, 160);
+      case 32056: AQR_LAUNCH_FP(32, 1, 56); case 32160: AQR_LAUNCH_FP(32, 1, 160);
       default: return cudaErrorInvalidValue;
     }
 #undef AQR_LAUNCH_FP
