@@ -35,6 +35,10 @@ namespace {
 #ifndef AQR_MIN_CTAS
 #define AQR_MIN_CTAS 6  // 6 CTAs x 4 warps (<= 85 regs): the shared-memory limit at ef ~ 800
 #endif
+#ifndef AQR_W_SLACK
+#define AQR_W_SLACK 0  // >0: free W slots before the list so an insert may move the head left instead of the
+                       // tail right (parity-tested; measured slower at C2: 15.2 vs 13.2 ms with 128)
+#endif
 #ifndef AQR_SEARCH4
 #define AQR_SEARCH4 0  // 1: 4-ary W lower bound (three probes per step; measured slower at throughput)
 #endif
@@ -193,7 +197,7 @@ struct Hot {
 Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   Layout L;
   int o = hot_bytes;
-  L.o_w = o; o += al16(8 * (c.ef + 1));
+  L.o_w = o; o += al16(8 * (c.ef + 1 + AQR_W_SLACK));
   // the query (codes + fp32) is only read before the beam and in Stage 2/3: when it fits it
   // borrows the beam's scratch (AQR traversal; the fp32 baseline reads it throughout)
   L.q_alias = !c.fp32 && al16(4 * ix.d4) + al16(ix.d_pad) <= hot_bytes;
@@ -787,7 +791,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
   uint8_t* wb = smem + (threadIdx.x >> 5) * L.per_warp;
   uint8_t* qc = wb + L.o_qc;
   float* qf = reinterpret_cast<float*>(wb + L.o_qf);
-  uint64_t* W = reinterpret_cast<uint64_t*>(wb + H::bytes);
+  uint64_t* const Wbase = reinterpret_cast<uint64_t*>(wb + H::bytes);
+  uint64_t* W = Wbase + AQR_W_SLACK;  // W[0] is Wbase[wstart]; set per query
   uint32_t* hash = reinterpret_cast<uint32_t*>(wb + L.o_h);
   int32_t* nb = reinterpret_cast<int32_t*>(wb + H::o_nb);
   int32_t* nd = reinterpret_cast<int32_t*>(wb + H::o_nd);
@@ -877,6 +882,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     }
 
     // 3. layer-0 beam (flag form)
+    int wstart = AQR_W_SLACK;
+    W = Wbase + wstart;
     if (INL) {
       if (lane == 0) {
         fence_proxy_async();
@@ -1065,14 +1072,68 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       for (int i = lane; i < np; i += 32) {
         const uint64_t kk = cand[i];
         int r = 0;
+#pragma unroll 4
         for (int j = 0; j < np; ++j) r += cand[j] < kk;
         cs[r] = kk;
         slb[r] = clb[i];
       }
       __syncwarp();
       const int first_ins = slb[0];
-      int seg_hi = size;
-      for (int j = np - 1; j >= 0; --j) {
+      // move whichever side of the insertion points is shorter: the entries after the first
+      // one right (tail), or those before the last one left into the free head slots (head)
+      bool head = AQR_W_SLACK > 0 && slb[np - 1] < size - first_ins && np <= AQR_W_SLACK;
+      if (head && wstart < np) {
+        // re-centre: the whole list moves right so the head has AQR_W_SLACK free slots again
+        const int sh = AQR_W_SLACK - wstart;
+        for (int hi = size; hi > 0; hi -= 128) {
+          const int lo = hi - 128 > 0 ? hi - 128 : 0;
+          const int nchk = (hi - lo + 31) >> 5;
+          uint64_t v[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int p = lo + 32 * t + lane;
+            if (t < nchk) v[t] = p < hi ? W[p] : 0ull;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int p = lo + 32 * t + lane;
+            if (t < nchk && p < hi) W[p + sh] = v[t];
+          }
+          __syncwarp();
+        }
+        W += sh;
+        wstart += sh;
+      }
+      if (head) {
+        // segment j = W[slb[j-1], slb[j]) (slb[-1] = 0) moves left by np - j, lowest first
+        int seg_lo = 0;
+        for (int j = 0; j < np; ++j) {
+          const int sh = np - j;
+          const int seg_hi2 = slb[j];
+          for (int lo = seg_lo; lo < seg_hi2; lo += 128) {
+            const int hi = lo + 128 < seg_hi2 ? lo + 128 : seg_hi2;
+            uint64_t v[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int p = lo + 32 * t + lane;
+              v[t] = p < hi ? W[p] : 0ull;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int p = lo + 32 * t + lane;
+              if (p < hi) W[p - sh] = v[t];
+            }
+            __syncwarp();
+          }
+          seg_lo = seg_hi2;
+        }
+        W -= np;
+        wstart -= np;
+      }
+      int seg_hi = head ? 0 : size;
+      for (int j = head ? -1 : np - 1; j >= 0; --j) {
         const int sh = j + 1;
         const int seg_lo = slb[j];
         for (int hi = seg_hi < ef - sh ? seg_hi : ef - sh; hi > seg_lo; hi -= 128) {
