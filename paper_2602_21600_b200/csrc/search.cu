@@ -641,6 +641,59 @@ __device__ __forceinline__ float exact_row(const IndexView& ix, const float* qf,
   return ix.metric == 0 ? acc : __fsub_rn(1.0f, acc);
 }
 
+// the same for up to four rows at once (rows with id < 0 give 0): the loads of all four rows
+// are in flight together; per row the arithmetic and its order are exactly asym_row's / exact_row's
+template <bool EXACT>
+__device__ __forceinline__ void rows4(const IndexView& ix, const float* qf, const int32_t (&id)[4], int lane,
+                                      float (&out)[4]) {
+  const int n4 = ix.d4 >> 2;
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  for (int c = lane; c < n4; c += 32) {
+    const float4 qv = reinterpret_cast<const float4*>(qf)[c];
+    float4 xv[4];
+    if (EXACT) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        xv[r] = id[r] >= 0 ? __ldg(reinterpret_cast<const float4*>(ix.base + (int64_t)id[r] * ix.d4) + c)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      uint32_t w[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        w[r] = id[r] >= 0 ? __ldg(reinterpret_cast<const uint32_t*>(ix.codes + (int64_t)id[r] * ix.d_pad) + c) : 0u;
+      const float4 sv = __ldg(reinterpret_cast<const float4*>(ix.scale_j) + c);
+      const float4 mv = __ldg(reinterpret_cast<const float4*>(ix.min_j) + c);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        xv[r].x = __fadd_rn(__fdiv_rn((float)(w[r] & 255u), sv.x), mv.x);
+        xv[r].y = __fadd_rn(__fdiv_rn((float)((w[r] >> 8) & 255u), sv.y), mv.y);
+        xv[r].z = __fadd_rn(__fdiv_rn((float)((w[r] >> 16) & 255u), sv.z), mv.z);
+        xv[r].w = __fadd_rn(__fdiv_rn((float)(w[r] >> 24), sv.w), mv.w);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (ix.metric == 0) {
+        float e;
+        e = __fsub_rn(qv.x, xv[r].x); acc[r] = __fmaf_rn(e, e, acc[r]);
+        e = __fsub_rn(qv.y, xv[r].y); acc[r] = __fmaf_rn(e, e, acc[r]);
+        e = __fsub_rn(qv.z, xv[r].z); acc[r] = __fmaf_rn(e, e, acc[r]);
+        e = __fsub_rn(qv.w, xv[r].w); acc[r] = __fmaf_rn(e, e, acc[r]);
+      } else {
+        acc[r] = __fmaf_rn(qv.x, xv[r].x, acc[r]);
+        acc[r] = __fmaf_rn(qv.y, xv[r].y, acc[r]);
+        acc[r] = __fmaf_rn(qv.z, xv[r].z, acc[r]);
+        acc[r] = __fmaf_rn(qv.w, xv[r].w, acc[r]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float a = warp_sum(acc[r]);
+    out[r] = ix.metric == 0 ? a : __fsub_rn(1.0f, a);
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // Stages 2 / ET / 3 / assembly for one query (Alg2 l.8-24).  cid[0:nc] in smem holds C in
 // (d^q, id) order; region holds >= 20*nc bytes of scratch after cid.
@@ -652,11 +705,18 @@ __device__ void finish_query(const IndexView& ix, const SearchCfg& c, const floa
                              int32_t* out_ids, float* out_dist, const aqr_debug& dbg, bool has_dbg, int lane,
                              int64_t* cnt) {
   // Stage 2: d^a for every entry of C (Alg2 l.10-12)
-  for (int i = 0; i < nc; ++i) {
-    const int32_t id = cid ? cid[i] : qkey_id(wk[i]);
-    const float da = asym_row(ix, qf, id, lane);
-    __syncwarp();
-    if (lane == 0) rkeys[i] = akey(da, id);
+  for (int i0 = 0; i0 < nc; i0 += 4) {
+    int32_t id[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) id[r] = i0 + r < nc ? (cid ? cid[i0 + r] : qkey_id(wk[i0 + r])) : -1;
+    float da[4];
+    rows4<false>(ix, qf, id, lane, da);
+    __syncwarp();  // wk may alias rkeys: these entries are read before they are overwritten
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (i0 + r < nc) rkeys[i0 + r] = akey(da[r], id[r]);
+    }
   }
   __syncwarp();
   // A <- sort by (d^a, id) (Alg2 l.13)
@@ -674,12 +734,20 @@ __device__ void finish_query(const IndexView& ix, const SearchCfg& c, const floa
   int depth = c.n_rerank < nc ? c.n_rerank : nc;
   if (term && depth > k) depth = k;
   // Stage 3: exact distances for A[0:depth] (Alg2 l.19-22)
-  for (int i = 0; i < depth; ++i) {
-    const int32_t id = (int32_t)(uint32_t)akeys[i];
-    const float de = exact_row(ix, qf, id, lane);
+  for (int i0 = 0; i0 < depth; i0 += 4) {
+    int32_t id[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) id[r] = i0 + r < depth ? (int32_t)(uint32_t)akeys[i0 + r] : -1;
+    float de[4];
+    rows4<true>(ix, qf, id, lane, de);
     if (lane == 0) {
-      rkeys[i] = akey(de, id);
-      if (has_dbg && dbg.exact_d) dbg.exact_d[qi * c.n_coarse + i] = de;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (i0 + r < depth) {
+          rkeys[i0 + r] = akey(de[r], id[r]);
+          if (has_dbg && dbg.exact_d) dbg.exact_d[qi * c.n_coarse + i0 + r] = de[r];
+        }
+      }
     }
   }
   // assembly (Alg2 l.23-24): R = R_exact U (fill: as needed for k / union: the rest of A)
