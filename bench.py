@@ -431,6 +431,24 @@ def run_aqr(args):
     e2e_ms = allreduce_max(e0.elapsed_time(e1) / args.steps, world)
     e2e_val = queries_per_step_all / (e2e_ms / 1e3)
 
+    # ---- optional steady-state stream: fresh queries, same index and parameters ----
+    steady = None
+    if args.stream > 0:
+        import synth
+        qs = torch.from_numpy(synth.gen_query_stream(cfg, args.stream)).cuda()
+        ss = aqr.Searcher(ix, len(qs), p)
+        ss.run(qs)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(3):
+            ss.run(qs)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        sms = allreduce_max(s0.elapsed_time(s1) / 3, world)
+        steady = {"queries_per_rank": len(qs), "qps": round(len(qs) * world / (sms / 1e3), 1),
+                  "ms_per_launch": round(sms, 3), "note": "fresh queries (stream 3), same index / ef"}
+
     # ---- roofline of the dominant kernel (search_kernel: one launch per step) ----
     import json as _json
     peaks = {}
@@ -482,6 +500,7 @@ def run_aqr(args):
                     "h2d_bytes_per_step": int(q_host.nbytes),
                     "d2h_bytes_per_step": int(ids_h.numel() * 4 + dist_h.numel() * 4)},
             "gpu_launches": args.steps,
+            "steady_state": steady,
             "clocks": clk,
             "ef_sweep": sweep,
             "counters_per_query": {n: round(float(v) / len(q), 2) for n, v in zip(aqr.COUNTER_NAMES, tot_counters)},
@@ -726,6 +745,8 @@ def main():
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--ef", default="auto")
     ap.add_argument("--full-sweep", action="store_true")
+    ap.add_argument("--stream", type=int, default=0,
+                    help="also time a steady-state stream of this many fresh queries (C1/C4 under-fill the GPU)")
     ap.add_argument("--traversal", default="aqr", choices=["aqr", "fp32"],
                     help="aqr: the method; fp32: the paper's baseline HNSW search on the same graph (NEXT-2)")
     ap.add_argument("--rerank", default="auto",

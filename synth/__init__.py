@@ -150,6 +150,25 @@ def gen_config(name: str, scale: float = 1.0, seed: int = 0, nq: int | None = No
     return w
 
 
+def gen_query_stream(name: str, nq: int, seed: int = 0) -> np.ndarray:
+    """Supplementary query stream (stream 3): fresh queries from the config's
+    distribution, for steady-state throughput where the config's own query set under-fills the
+    GPU (C1: 100 queries, C4: 1k).  Recall is always measured on the config's query set."""
+    r = _rng(seed, name, 3)
+    if name == "C1":
+        c, s = _mixture_params(seed, "C1", 128, 16, 0.05, 1.0)
+        return _gmm(r, nq, 128, 16, 0, 0, c, s)
+    if name == "C2":
+        return _gamma_int(r, nq, 128)
+    if name == "C3":
+        return _aniso_unit(r, nq, 100)
+    if name == "C4":
+        c, s = _mixture_params(seed, "C4", 960, 64, 0.02, 0.5)
+        return np.abs(_gmm(r, nq, 960, 64, 0, 0, c, s, chunk=1 << 16))
+    c, s = _mixture_params(seed, "C5", 96, 1024, 0.01, 1.0)
+    return _gmm(r, nq, 96, 1024, 0, 0, c, s)
+
+
 # ---------------------------------------------------------------------------------
 # small fixtures
 # ---------------------------------------------------------------------------------
