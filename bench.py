@@ -56,8 +56,17 @@ def dist_init(n_gpus):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one process per GPU over NCCL.  AQR_DIST_BACKEND=gloo runs the same multi-rank code path
+        # with several ranks sharing a device (a functional check of the N > 1 plumbing on a
+        # one-GPU box; never a measurement: the ranks time-share the GPU)
+        backend = os.environ.get("AQR_DIST_BACKEND", "nccl")
+        dev = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+        local = dev
     else:
         torch.cuda.set_device(0)
     return rank, world, local

@@ -35,6 +35,9 @@ namespace {
 #ifndef AQR_MIN_CTAS
 #define AQR_MIN_CTAS 6  // 6 CTAs x 4 warps (<= 85 regs): the shared-memory limit at ef ~ 800
 #endif
+#ifndef AQR_SHORT_SEG
+#define AQR_SHORT_SEG 0  // 1: one-chunk fast path for W segments of <= 32 entries (measured neutral)
+#endif
 #ifndef AQR_W_SLACK
 #define AQR_W_SLACK 0  // >0: free W slots before the list so an insert may move the head left instead of the
                        // tail right (parity-tested; measured slower at C2: 15.2 vs 13.2 ms with 128)
@@ -200,22 +203,30 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   L.o_w = o; o += al16(8 * (c.ef + 1 + AQR_W_SLACK));
   // the query (codes + fp32) is only read before the beam and in Stage 2/3: when it fits it
   // borrows the beam's scratch (AQR traversal; the fp32 baseline reads it throughout)
-  L.q_alias = !c.fp32 && al16(4 * ix.d4) + al16(ix.d_pad) <= hot_bytes;
-  if (L.q_alias) {
-    L.o_qf = 0;
-    L.o_qc = al16(4 * ix.d4);
-  } else {
-    L.o_qc = o; o += al16(ix.d_pad);
-    L.o_qf = o; o += al16(4 * ix.d4);
-  }
+  const int qbytes = al16(4 * ix.d4) + al16(ix.d_pad);
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
   L.region = ix.blk ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
   if (c.staged) {  // staged_dists: 2 x kStage wide rows
     const int st = 2 * kStage * ix.d_pad;
     if (st > L.region) L.region = st;
   }
+  // ... or the staged gather's buffer (wide rows: the query is too big for the hot arrays)
+  const bool in_hot = !c.fp32 && qbytes <= hot_bytes;
+  const bool in_stage = !c.fp32 && !in_hot && c.staged && !ix.blk && c.hbits == 0 && qbytes <= L.region;
+  L.q_alias = in_hot || in_stage;
+  if (!L.q_alias) {
+    L.o_qc = o; o += al16(ix.d_pad);
+    L.o_qf = o; o += al16(4 * ix.d4);
+  }
   o = (o + 127) & ~127;
   L.o_h = o; o += al16(L.region);
+  if (in_hot) {
+    L.o_qf = 0;
+    L.o_qc = al16(4 * ix.d4);
+  } else if (in_stage) {
+    L.o_qf = L.o_h;
+    L.o_qc = L.o_h + al16(4 * ix.d4);
+  }
   L.o_s23 = o; o += c.ef >= 2 * c.n_coarse ? 0 : al16(8 * c.n_coarse);
   L.per_warp = (o + 127) & ~127;
   return L;
@@ -1204,7 +1215,22 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       for (int j = head ? -1 : np - 1; j >= 0; --j) {
         const int sh = j + 1;
         const int seg_lo = slb[j];
-        for (int hi = seg_hi < ef - sh ? seg_hi : ef - sh; hi > seg_lo; hi -= 128) {
+        int hi = seg_hi < ef - sh ? seg_hi : ef - sh;
+#if AQR_SHORT_SEG
+        if (hi - seg_lo <= 32) {
+          // short segment (the common case): one chunk
+          if (hi > seg_lo) {
+            const int p = seg_lo + lane;
+            const uint64_t v0 = p < hi ? W[p] : 0ull;
+            __syncwarp();
+            if (p < hi) W[p + sh] = v0;
+            __syncwarp();
+          }
+          seg_hi = seg_lo;
+          continue;
+        }
+#endif
+        for (; hi > seg_lo; hi -= 128) {
           const int lo = hi - 128 > seg_lo ? hi - 128 : seg_lo;
           uint64_t v[4];
 #pragma unroll
