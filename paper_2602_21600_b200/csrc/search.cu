@@ -35,6 +35,9 @@ namespace {
 #ifndef AQR_MIN_CTAS
 #define AQR_MIN_CTAS 6  // 6 CTAs x 4 warps (<= 85 regs): the shared-memory limit at ef ~ 800
 #endif
+#ifndef AQR_L2HINT
+#define AQR_L2HINT 1  // L2 eviction hints: code rows evict-last, adjacency rows evict-first
+#endif
 #ifndef AQR_SHORT_SEG
 #define AQR_SHORT_SEG 0  // 1: one-chunk fast path for W segments of <= 32 entries (measured neutral)
 #endif
@@ -278,6 +281,43 @@ __device__ __forceinline__ void ldg256(const void* p, C32& v) {
                : "l"(p));
 }
 
+// the same with an L2 evict-last hint (LDG.E.NA.ELL2.256): the code rows are the data reused
+// across queries, so they should outlive the adjacency rows and fp32 rows in L2
+__device__ __forceinline__ void ldg256_keep(const void* p, C32& v) {
+#if AQR_L2HINT
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.a.x), "=r"(v.a.y), "=r"(v.a.z), "=r"(v.a.w), "=r"(v.b.x), "=r"(v.b.y), "=r"(v.b.z),
+                 "=r"(v.b.w)
+               : "l"(p));
+#else
+  ldg256(p, v);
+#endif
+}
+
+// scalar loads with an L2 eviction policy (createpolicy + L2::cache_hint)
+__device__ __forceinline__ int32_t ldg_first(const int32_t* p) {
+#if AQR_L2HINT
+  uint64_t pol;
+  int32_t v;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ int32_t ldg_last(const int32_t* p) {
+#if AQR_L2HINT
+  uint64_t pol;
+  int32_t v;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ void dp4a_c32(const C32& w, const C32& q, unsigned& xx, unsigned& qx) {
   xx = __dp4a(w.a.x, w.a.x, xx); qx = __dp4a(q.a.x, w.a.x, qx);
   xx = __dp4a(w.a.y, w.a.y, xx); qx = __dp4a(q.a.y, w.a.y, qx);
@@ -346,7 +386,7 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg
       const int u = U >= LPR ? sub * PER + v : sub / REP;
       const int r = r0 + g * U + u;
       const int id = r < m ? ids[r] : -1;
-      xn[v] = id >= 0 ? __ldg(ix.xnorm + id) : 0;
+      xn[v] = id >= 0 ? ldg_last(ix.xnorm + id) : 0;
     }
     C32 buf[U][CPL];
 #pragma unroll
@@ -358,7 +398,7 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg
       for (int t = 0; t < CPL; ++t) {
         const int c = sub + LPR * t;
         if (id >= 0 && c < nch) {
-          ldg256(row + 32 * c, buf[u][t]);
+          ldg256_keep(row + 32 * c, buf[u][t]);
         } else {
           buf[u][t].a = make_uint4(0, 0, 0, 0);
           buf[u][t].b = make_uint4(0, 0, 0, 0);
@@ -598,62 +638,10 @@ __device__ __forceinline__ float warp_sum(float a) {
   return a;
 }
 
-__device__ __forceinline__ float asym_row(const IndexView& ix, const float* qf, int32_t id, int lane) {
-  const uint8_t* crow = ix.codes + (int64_t)id * ix.d_pad;
-  const int n4 = ix.d4 >> 2;
-  float acc = 0.0f;
-  for (int c = lane; c < n4; c += 32) {
-    const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(crow) + c);
-    const float4 qv = reinterpret_cast<const float4*>(qf)[c];
-    const float4 sv = __ldg(reinterpret_cast<const float4*>(ix.scale_j) + c);
-    const float4 mv = __ldg(reinterpret_cast<const float4*>(ix.min_j) + c);
-    const float x0 = __fadd_rn(__fdiv_rn((float)(w & 255u), sv.x), mv.x);
-    const float x1 = __fadd_rn(__fdiv_rn((float)((w >> 8) & 255u), sv.y), mv.y);
-    const float x2 = __fadd_rn(__fdiv_rn((float)((w >> 16) & 255u), sv.z), mv.z);
-    const float x3 = __fadd_rn(__fdiv_rn((float)(w >> 24), sv.w), mv.w);
-    if (ix.metric == 0) {
-      float e;
-      e = __fsub_rn(qv.x, x0); acc = __fmaf_rn(e, e, acc);
-      e = __fsub_rn(qv.y, x1); acc = __fmaf_rn(e, e, acc);
-      e = __fsub_rn(qv.z, x2); acc = __fmaf_rn(e, e, acc);
-      e = __fsub_rn(qv.w, x3); acc = __fmaf_rn(e, e, acc);
-    } else {
-      acc = __fmaf_rn(qv.x, x0, acc);
-      acc = __fmaf_rn(qv.y, x1, acc);
-      acc = __fmaf_rn(qv.z, x2, acc);
-      acc = __fmaf_rn(qv.w, x3, acc);
-    }
-  }
-  acc = warp_sum(acc);
-  return ix.metric == 0 ? acc : __fsub_rn(1.0f, acc);
-}
-
-__device__ __forceinline__ float exact_row(const IndexView& ix, const float* qf, int32_t id, int lane) {
-  const float4* xrow = reinterpret_cast<const float4*>(ix.base + (int64_t)id * ix.d4);
-  const int n4 = ix.d4 >> 2;
-  float acc = 0.0f;
-  for (int c = lane; c < n4; c += 32) {
-    const float4 xv = __ldg(xrow + c);
-    const float4 qv = reinterpret_cast<const float4*>(qf)[c];
-    if (ix.metric == 0) {
-      float e;
-      e = __fsub_rn(qv.x, xv.x); acc = __fmaf_rn(e, e, acc);
-      e = __fsub_rn(qv.y, xv.y); acc = __fmaf_rn(e, e, acc);
-      e = __fsub_rn(qv.z, xv.z); acc = __fmaf_rn(e, e, acc);
-      e = __fsub_rn(qv.w, xv.w); acc = __fmaf_rn(e, e, acc);
-    } else {
-      acc = __fmaf_rn(qv.x, xv.x, acc);
-      acc = __fmaf_rn(qv.y, xv.y, acc);
-      acc = __fmaf_rn(qv.z, xv.z, acc);
-      acc = __fmaf_rn(qv.w, xv.w, acc);
-    }
-  }
-  acc = warp_sum(acc);
-  return ix.metric == 0 ? acc : __fsub_rn(1.0f, acc);
-}
-
-// the same for up to four rows at once (rows with id < 0 give 0): the loads of all four rows
-// are in flight together; per row the arithmetic and its order are exactly asym_row's / exact_row's
+// four rows at once (rows with id < 0 give 0), their loads in flight together.  Per row: lanes own
+// 4-wide chunks c = lane + 32 t, one FMA per term in increasing c, then a butterfly sum.
+// Stage 2 (EXACT = false) decodes the codes x~ = x^ / scale + min (IEEE division, Alg2 l.11);
+// Stage 3 (EXACT = true) reads the fp32 row.
 template <bool EXACT>
 __device__ __forceinline__ void rows4(const IndexView& ix, const float* qf, const int32_t (&id)[4], int lane,
                                       float (&out)[4]) {
@@ -1133,7 +1121,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
           for (int t = 0; t < kRowRegs; ++t) {
             const int j = lane + 32 * t;
             arow[t] = -1;
-            if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = __ldg(ix.adj0 + rb + j);
+            if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = ldg_first(ix.adj0 + rb + j);
           }
         }
       }
