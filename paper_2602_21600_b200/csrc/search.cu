@@ -35,6 +35,10 @@ namespace {
 #ifndef AQR_MIN_CTAS
 #define AQR_MIN_CTAS 6  // 6 CTAs x 4 warps (<= 85 regs): the shared-memory limit at ef ~ 800
 #endif
+#ifndef AQR_SPEC2
+#define AQR_SPEC2 0  // 1: row of the likely next expansion loaded early, its codes prefetched to L2
+                     // (measured slower, 13.9 vs 12.8 ms, and no single-query latency gain)
+#endif
 #ifndef AQR_BALANCE
 #define AQR_BALANCE 0  // 1: grid sized so every warp serves the same number of queries (measured
                        // slower, 13.3 vs 12.8 ms: the extra warps of a partial round still hide latency)
@@ -980,6 +984,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     // expansion right after the filter so the load overlaps the merge
     constexpr int kRowRegs = 5;  // cap0 = 2M <= 160 (ABI: M <= 80)
     int32_t arow[kRowRegs];
+    int32_t arow2[kRowRegs];  // AQR_SPEC2: row of the guessed expansion after next
     if (!INL) {
 #pragma unroll
       for (int t = 0; t < kRowRegs; ++t) {
@@ -991,14 +996,33 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     int size = 1, cursor = 0, nexp = 0;
     for (;;) {
       // smallest unexpanded entry of W
-      int pos = -1;
+      int pos = -1, gpos = -1;
       for (int bb = cursor; bb < size; bb += 32) {
         const int i = bb + lane;
         const bool un = i < size && !(W[i] & 1ull);
         const uint32_t mk = __ballot_sync(kFull, un);
-        if (mk) { pos = bb + __ffs(mk) - 1; break; }
+        if (mk) {
+          pos = bb + __ffs(mk) - 1;
+          const uint32_t mk2 = mk & (mk - 1);
+          if (mk2) gpos = bb + __ffs(mk2) - 1;
+          break;
+        }
       }
       if (pos < 0) break;
+      // AQR_SPEC2: the next unexpanded entry is the following expansion unless this one inserts
+      // a smaller key (~80% of expansions): load its row now, so that if it IS next its code
+      // rows can be prefetched into L2 before this expansion's insert (side-effect free)
+      int32_t spec = -1;
+      if (!INL && AQR_SPEC2 && gpos >= 0) {
+        spec = qkey_id(W[gpos]);
+        const int64_t rb2 = (int64_t)spec * ix.ld0;
+#pragma unroll
+        for (int t = 0; t < kRowRegs; ++t) {
+          const int j = lane + 32 * t;
+          arow2[t] = -1;
+          if (32 * t < ix.cap0 && j < ix.cap0) arow2[t] = __ldg(ix.adj0 + rb2 + j);
+        }
+      }
       const uint64_t wk = W[pos];
       const int32_t cnode = qkey_id(wk);
       __syncwarp();
@@ -1121,12 +1145,25 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
             bulk_load(blkbuf, ix.blk + (int64_t)qkey_id(nxt) * ix.blk_stride, (uint32_t)ix.blk_bytes, bar);
           }
         } else if (AQR_PREFETCH_ROW && nxt != ~0ull) {
-          const int64_t rb = (int64_t)qkey_id(nxt) * ix.ld0;
+          if (spec >= 0 && qkey_id(nxt) == spec) {
+            // guessed right: the row is here; pull its neighbours' code rows into L2 now
+            const int lines = (ix.d_pad + 127) >> 7;
 #pragma unroll
-          for (int t = 0; t < kRowRegs; ++t) {
-            const int j = lane + 32 * t;
-            arow[t] = -1;
-            if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = ldg_first(ix.adj0 + rb + j);
+            for (int t = 0; t < kRowRegs; ++t) {
+              arow[t] = arow2[t];
+              if (32 * t < ix.cap0 && arow[t] >= 0) {
+                const uint8_t* cr = ix.codes + (int64_t)arow[t] * ix.d_pad;
+                for (int l = 0; l < lines; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(cr + 128 * l));
+              }
+            }
+          } else {
+            const int64_t rb = (int64_t)qkey_id(nxt) * ix.ld0;
+#pragma unroll
+            for (int t = 0; t < kRowRegs; ++t) {
+              const int j = lane + 32 * t;
+              arow[t] = -1;
+              if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = ldg_first(ix.adj0 + rb + j);
+            }
           }
         }
       }
