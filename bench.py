@@ -583,8 +583,23 @@ def run_sharded(args):
         if rank == 0:
             log(f"[bench] C5 shard {s_}: {infos[-1]}")
 
+    # the shards of a rank are searched concurrently on their own streams, so the persistent
+    # grids of consecutive shards overlap instead of each launch paying its own tail
+    side = [torch.cuda.Stream() for _ in shards] if args.shard_streams and len(shards) > 1 else None
+
     def step():
-        outs = [sh[2].run(q) for sh in shards]
+        if side is None:
+            outs = [sh[2].run(q) for sh in shards]
+        else:
+            main = torch.cuda.current_stream()
+            ready = torch.cuda.Event()
+            ready.record(main)
+            outs = []
+            for sh, st in zip(shards, side):
+                st.wait_event(ready)
+                outs.append(sh[2].run(q, stream=st))
+            for st in side:
+                main.wait_stream(st)
         if len(outs) == 1:
             ld, li = outs[0][1], outs[0][0]
         else:
@@ -754,6 +769,8 @@ def main():
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--ef", default="auto")
     ap.add_argument("--full-sweep", action="store_true")
+    ap.add_argument("--shard-streams", type=int, default=1,
+                    help="C5: search a rank's shards concurrently on separate CUDA streams (1) or one after another (0)")
     ap.add_argument("--stream", type=int, default=0,
                     help="also time a steady-state stream of this many fresh queries (C1/C4 under-fill the GPU)")
     ap.add_argument("--traversal", default="aqr", choices=["aqr", "fp32"],

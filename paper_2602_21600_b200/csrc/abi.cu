@@ -75,8 +75,21 @@ aqr_status aqr_encode(const float* x, int64_t n, int32_t d, int64_t ld_x, const 
     double* meta = nullptr;
     double* rho = nullptr;
     void* tmp = nullptr;
-    AQR_CUDA(cudaMallocAsync((void**)&meta, 4 * sizeof(double), s), "encode: alloc");
     const bool need_rho = std::isnan(train->delta_override) || train->rho_out;
+    // temporaries are released on every exit path (stream-ordered), including errors
+    struct Tmp {
+      double*& meta;
+      double*& rho;
+      void*& tmp;
+      bool own_rho;
+      cudaStream_t s;
+      ~Tmp() {
+        if (tmp) cudaFreeAsync(tmp, s);
+        if (meta) cudaFreeAsync(meta, s);
+        if (own_rho && rho) cudaFreeAsync(rho, s);
+      }
+    } guard{meta, rho, tmp, need_rho && !train->rho_out, s};
+    AQR_CUDA(cudaMallocAsync((void**)&meta, 4 * sizeof(double), s), "encode: alloc");
     if (need_rho) {
       rho = train->rho_out;
       if (!rho) AQR_CUDA(cudaMallocAsync((void**)&rho, sizeof(double) * train->n_sample, s), "encode: alloc");
@@ -92,9 +105,6 @@ aqr_status aqr_encode(const float* x, int64_t n, int32_t d, int64_t ld_x, const 
              "encode: percentile kernels");
     double hmeta[4] = {0, 0, 0, 0};
     AQR_CUDA(cudaMemcpyAsync(hmeta, meta, 3 * sizeof(double), cudaMemcpyDeviceToHost, s), "encode: copy");
-    AQR_CUDA(cudaFreeAsync(tmp, s), "encode: free");
-    AQR_CUDA(cudaFreeAsync(meta, s), "encode: free");
-    if (need_rho && !train->rho_out) AQR_CUDA(cudaFreeAsync(rho, s), "encode: free");
     AQR_CUDA(cudaStreamSynchronize(s), "encode: sync");
     qp->delta = hmeta[0];
     qp->p_low = hmeta[1];
