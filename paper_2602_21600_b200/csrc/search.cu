@@ -35,6 +35,9 @@ namespace {
 #ifndef AQR_MIN_CTAS
 #define AQR_MIN_CTAS 6  // 6 CTAs x 4 warps (<= 85 regs): the shared-memory limit at ef ~ 800
 #endif
+#ifndef AQR_NOCOMPACT
+#define AQR_NOCOMPACT 1  // GATHER without the visited hash: score the adjacency row as stored
+#endif
 #ifndef AQR_SPEC2
 #define AQR_SPEC2 0  // 1: row of the likely next expansion loaded early, its codes prefetched to L2
                      // (measured slower, 13.9 vs 12.8 ms, and no single-query latency gain)
@@ -1062,21 +1065,34 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         }
         int deg = 0;
         m = 0;
+        if (AQR_NOCOMPACT && !vhash) {
+          // the row as it is: -1 entries are skipped by the gather and the filter
+          m = ix.cap0;
 #pragma unroll
-        for (int t = 0; t < kRowRegs; ++t) {
-          if (32 * t >= ix.cap0) break;  // uniform
-          const int32_t u = arow[t];
-          deg += __popc(__ballot_sync(kFull, u >= 0));
-          bool keep = u >= 0;
-          if (keep && vhash) keep = visit_new(hash, c.hbits, u, fails);
-          const uint32_t mk = __ballot_sync(kFull, keep);
-          if (keep) nb[m + __popc(mk & ((1u << lane) - 1u))] = u;
-          m += __popc(mk);
+          for (int t = 0; t < kRowRegs; ++t)
+            if (32 * t < ix.cap0) nb[lane + 32 * t] = arow[t];
+          if (has_dbg) {
+#pragma unroll
+            for (int t = 0; t < kRowRegs; ++t)
+              if (32 * t < ix.cap0) deg += __popc(__ballot_sync(kFull, arow[t] >= 0));
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < kRowRegs; ++t) {
+            if (32 * t >= ix.cap0) break;  // uniform
+            const int32_t u = arow[t];
+            deg += __popc(__ballot_sync(kFull, u >= 0));
+            bool keep = u >= 0;
+            if (keep && vhash) keep = visit_new(hash, c.hbits, u, fails);
+            const uint32_t mk = __ballot_sync(kFull, keep);
+            if (keep) nb[m + __popc(mk & ((1u << lane) - 1u))] = u;
+            m += __popc(mk);
+          }
         }
         __syncwarp();
         ids = nb;
         cnt[1] += deg;
-        cnt[2] += m;
+        cnt[2] += (AQR_NOCOMPACT && !vhash) ? deg : m;
         dists(nb, m, nd);
       }
       __syncwarp();
