@@ -1,24 +1,27 @@
 // search.cu -- fused AQR-HNSW query search on sm_100a (aqr_search / aqr_rerank).
 //
-// One warp per query, persistent grid (atomic query counter).  Per query, all inside the
-// kernel (Alg2):
-//   1. quantize the query (Alg2 l.4) into shared memory;
+// One warp per query, persistent grid (atomic query counter), 24 warps per SM.  Per query,
+// all inside the kernel (Alg2):
+//   1. quantize the query (Alg2 l.4);
 //   2. greedy descent through layers max_level..1 on d^q (R8);
 //   3. layer-0 beam with ef on d^q (Alg2 l.6-7), "flag form" (R8): W is a sorted
 //      list of <= ef 64-bit keys (d^q << 32 | id << 1 | expanded) in shared memory; each step
-//      expands the smallest unexpanded entry, gathers its adjacency row, tests a visited
-//      hash in shared memory, gathers the unvisited codes with 16-byte loads (LPR lanes per
-//      code row), scores them with dp4a in int32, filters against max W and merges the
-//      survivors with a rank-based parallel merge;
+//      expands the smallest unexpanded entry: its adjacency row (requested during the previous
+//      insert) -> its neighbours' code rows gathered with 256-bit loads (LPR lanes per row) ->
+//      d^q = |q^|^2 + |x^|^2 - 2 q^.x^ with dp4a (|x^|^2 precomputed per node) -> filter
+//      against max W -> dedupe + insertion point by binary search in W -> insert (per-segment
+//      block moves); wide rows (d_pad > 512) are staged by TMA bulk copies instead;
 //   4. Stage 2: decode + asymmetric fp32 distance for C = W[0:N_c] (Alg2 l.8-13);
 //   5. early termination (Alg2 l.15-16, fp64 test on fp32 values, R11);
 //   6. Stage 3: exact fp32 distance over the retained fp32 rows (Alg2 l.18-22, FMA P:197);
 //   7. assembly + top-k (Alg2 l.23-24; fill reading R10 or union S:515) and the store.
+// traversal = fp32 (template FP) is the paper's baseline HNSW on the same graph (R22).
 //
 // The path is a gather (pointer chasing), not a contraction: no tensor cores (north_star).
 // Integer results (codes, d^q, W, visit order, ids) are bit-exact with the oracle; fp32
 // sums use a lane-strided FMA order and agree with the oracle's sequential order within
-// 1e-5 relative (north_star tolerance).
+// 1e-5 relative (north_star tolerance); the fp32 baseline uses the canonical order R(L) and
+// is bit-exact.  Compile-time AQR_* knobs below record measured alternatives.
 #include <cfloat>
 #include <climits>
 
