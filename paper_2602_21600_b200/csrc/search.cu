@@ -200,6 +200,10 @@ __host__ __device__ constexpr int rows_u() {
   return AQR_ROWS_PER_PASS / (2 * CPL) < 4 ? 4 : AQR_ROWS_PER_PASS / (2 * CPL) / 4 * 4;
 }
 
+// per-query counters + mbarriers at the end of the hot region: live for the whole kernel, so a
+// query aliased into the hot region (make_layout) stops short of them
+constexpr int kHotTail = 80;
+
 // the beam's per-warp scratch for adjacency rows of up to CAP entries (CAP = 56 or 160)
 template <int LPR, int CPL, int CAP>
 struct Hot {
@@ -211,8 +215,10 @@ struct Hot {
   static constexpr int o_cand = o_nd + al16(4 * CAP);       // u64 [CAP] new W keys
   static constexpr int o_cs = o_cand + 8 * CAP;             // u64 [CAP] survivors / sorted keys
   static constexpr int o_lb = o_cs + 8 * CAP;               // int32 [CAP] W lower bounds
-  static constexpr int o_bar = o_lb + al16(4 * CAP);        // mbarrier (INLINE)
+  static constexpr int o_cnt = o_lb + al16(4 * CAP);        // int32 [16] per-query counters (debug)
+  static constexpr int o_bar = o_cnt + 64;                  // mbarriers (INLINE / staged)
   static constexpr int bytes = o_bar + 16;                  // W follows
+  static_assert(bytes - o_cnt == kHotTail, "hot tail");
 };
 
 Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
@@ -229,7 +235,8 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
     if (st > L.region) L.region = st;
   }
   // ... or the staged gather's buffer (wide rows: the query is too big for the hot arrays)
-  const bool in_hot = !c.fp32 && qbytes <= hot_bytes;
+  // (the counters and mbarriers at the end of the hot region stay live: the query stops short)
+  const bool in_hot = !c.fp32 && qbytes <= hot_bytes - kHotTail;
   const bool in_stage = !c.fp32 && !in_hot && c.staged && !ix.blk && c.hbits == 0 && qbytes <= L.region;
   L.q_alias = in_hot || in_stage;
   if (!L.q_alias) {
@@ -717,7 +724,7 @@ __device__ __forceinline__ void rows4(const IndexView& ix, const float* qf, cons
 __device__ void finish_query(const IndexView& ix, const SearchCfg& c, const float* qf, const int32_t* cid,
                              const uint64_t* wk, int nc, uint64_t* akeys, uint64_t* rkeys, int64_t qi,
                              int32_t* out_ids, float* out_dist, const aqr_debug& dbg, bool has_dbg, int lane,
-                             int64_t* cnt) {
+                             int32_t* cnt) {
   // Stage 2: d^a for every entry of C (Alg2 l.10-12)
   for (int i0 = 0; i0 < nc; i0 += 4) {
     int32_t id[4];
@@ -882,6 +889,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
   uint64_t* cs = reinterpret_cast<uint64_t*>(wb + H::o_cs);
   uint64_t* bar = reinterpret_cast<uint64_t*>(wb + H::o_bar);
   int32_t* clb = reinterpret_cast<int32_t*>(wb + H::o_lb);
+  int32_t* scnt = reinterpret_cast<int32_t*>(wb + H::o_cnt);
   uint8_t* blkbuf = wb + L.o_h;
   uint32_t* vhash = c.hbits > 0 ? hash : nullptr;
   const int sub = lane % LPR;
@@ -905,9 +913,13 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     if (lane == 0) qi = atomicAdd(counter, 1);
     qi = __shfl_sync(kFull, qi, 0);
     if (qi >= nq) break;
-    int64_t cnt[AQR_NCOUNT];
+    // per-query counters live in shared memory and are only touched when a trace was requested,
+    // so they cost no registers on the timed path
+    int32_t* cnt = has_dbg ? scnt : nullptr;
+    if (cnt && lane == 0) {
 #pragma unroll
-    for (int t = 0; t < AQR_NCOUNT; ++t) cnt[t] = 0;
+      for (int t = 0; t < AQR_NCOUNT; ++t) cnt[t] = 0;
+    }
     int fails = 0;
 
     // 1. quantize the query
@@ -939,7 +951,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     dists(nb, 1, nd);
     __syncwarp();
     uint32_t dcur = (uint32_t)nd[0];
-    cnt[5] += 1;
+    if (cnt && lane == 0) cnt[5] += 1;
     for (int lv = ix.max_level; lv >= 1; --lv) {
       for (;;) {
         __syncwarp();
@@ -954,9 +966,9 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
           best = kk < best ? kk : best;
         }
         best = warp_min_u64(best);
-        cnt[3] += 1;
-        cnt[4] += deg;
-        cnt[5] += m;
+        if (cnt && lane == 0) cnt[3] += 1;
+        if (cnt && lane == 0) cnt[4] += deg;
+        if (cnt && lane == 0) cnt[5] += m;
         if (qkey_id(best) == cur) break;
         cur = qkey_id(best);
         dcur = qkey_d(best);
@@ -1052,8 +1064,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
           deg += __popc(__ballot_sync(kFull, u >= 0));
         }
         ids = nb;
-        cnt[1] += deg;
-        cnt[2] += deg;
+        if (cnt && lane == 0) cnt[1] += deg;
+        if (cnt && lane == 0) cnt[2] += deg;
         block_dists<LPR, CPL>(blkbuf + ix.blk_ids, ix.d_pad, qreg, qq, reinterpret_cast<const int32_t*>(blkbuf), m,
                               nd, lane);
       } else {
@@ -1094,8 +1106,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         }
         __syncwarp();
         ids = nb;
-        cnt[1] += deg;
-        cnt[2] += (AQR_NOCOMPACT && !vhash) ? deg : m;
+        if (cnt && lane == 0) cnt[1] += deg;
+        if (cnt && lane == 0) cnt[2] += (AQR_NOCOMPACT && !vhash) ? deg : m;
         dists(nb, m, nd);
       }
       __syncwarp();
@@ -1139,8 +1151,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         }
         np += __popc(mk);
       }
-      cnt[11] += np0;
-      cnt[12] += np;
+      if (cnt && lane == 0) cnt[11] += np0;
+      if (cnt && lane == 0) cnt[12] += np;
       {
         // the next expansion is min(first unexpanded entry of W after pos, smallest candidate);
         // start loading its layer-0 data now so the load overlaps the merge (prefetch only,
@@ -1304,8 +1316,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       size = size + np < ef ? size + np : ef;
       cursor = first_ins < pos + 1 ? first_ins : pos + 1;
     }
-    cnt[0] = nexp;
-    cnt[10] = fails;
+    if (cnt && lane == 0) cnt[0] = nexp;
+    if (cnt && lane == 0) cnt[10] = fails;
 
     // debug: C with d^q
     const int nc = c.n_coarse < size ? c.n_coarse : size;
