@@ -179,7 +179,7 @@ def make_workload(cfg, scale, nq):
     return synth.gen_config(cfg, scale=scale, nq=nq)
 
 
-def build_index(w, cfg, rank, world, threads):
+def build_index(w, cfg, rank, world, threads, delta_override=None):
     import torch
     import synth
     import paper_2602_21600_b200 as aqr
@@ -188,7 +188,7 @@ def build_index(w, cfg, rank, world, threads):
     x = torch.from_numpy(w.x).cuda()
     sample_np = synth.density_sample(len(w.x), seed=w.seed, cfg=cfg)
     sample = torch.from_numpy(sample_np).cuda()
-    codes, quant = aqr.encode(x, sample_idx=sample, p_max=P_MAX[cfg], want_rho=True)
+    codes, quant = aqr.encode(x, sample_idx=sample, p_max=P_MAX[cfg], want_rho=True, delta_override=delta_override)
     torch.cuda.synchronize()
     t_enc = time.time() - t0
     rho = quant.rho.cpu().numpy()
@@ -231,14 +231,14 @@ def bytes_per_query(tot, nq, d, k, distinct_ratio=1.0, traversal="aqr"):
     return b / nq
 
 
-def oracle_index(w, cfg, codes, g):
+def oracle_index(w, cfg, codes, g, delta_override=float("nan")):
     """The oracle trains its own quantizer and encodes the base itself (full-size parity check
     of aqr_encode: codes compared byte for byte), then searches the same graph."""
     import oracle
     import synth
     t0 = time.time()
     sample = synth.density_sample(len(w.x), seed=w.seed, cfg=cfg)
-    o_quant = oracle.train(w.x, sample, p_max=P_MAX[cfg])
+    o_quant = oracle.train(w.x, sample, p_max=P_MAX[cfg], delta_override=delta_override)
     o_codes = oracle.encode(w.x, o_quant)
     codes_equal = bool(np.array_equal(o_codes, codes.cpu().numpy()))
     return oracle.Index(w.x, o_codes, o_quant, g, w.metric), codes_equal, time.time() - t0
@@ -270,7 +270,8 @@ def run_aqr(args):
         lo, hi = 0, nq  # weak scaling: every rank searches the full query set
     q_host = np.ascontiguousarray(w.q[lo:hi])
     q = torch.from_numpy(q_host).cuda()
-    x, codes, quant, g, ix, info = build_index(w, cfg, rank, world, args.threads)
+    sq8 = args.traversal == "sq8"
+    x, codes, quant, g, ix, info = build_index(w, cfg, rank, world, args.threads, 0.0 if sq8 else None)
     if rank == 0:
         log(f"[bench] {cfg} n={len(w.x)} d={w.x.shape[1]} nq={nq} index: {info}")
 
@@ -286,13 +287,15 @@ def run_aqr(args):
         mm = aqr.ef_mapping(ef, k)
         if args.traversal == "fp32":  # the baseline: W's first k are the result
             return dict(ef=max(ef, k), n_coarse=k, n_rerank=k)
-        if mode == "full":
+        if mode == "full" or sq8:
             mm["n_rerank"] = mm["n_coarse"]
+        if sq8:  # plain SQ8 HNSW (R23): no early termination, every C entry re-ranked exactly
+            mm["early_term"] = False
         return mm
 
     def measure(ef, mode):
         m = mapping(ef, mode)
-        p = aqr.make_params(k, **m, visited_bits=args.vbits[0], traversal=args.traversal)
+        p = aqr.make_params(k, **m, visited_bits=args.vbits[0], traversal=args.kt)
         s = aqr.Searcher(ix, len(q), p)
         s.run(q)
         torch.cuda.synchronize()
@@ -356,7 +359,7 @@ def run_aqr(args):
     vb_results = []
     best_vb, best_ms = 0, float("inf")
     for vb in args.vbits:
-        p = aqr.make_params(k, **m, visited_bits=vb, traversal=args.traversal)
+        p = aqr.make_params(k, **m, visited_bits=vb, traversal=args.kt)
         s = aqr.Searcher(ix, len(q), p)
         s.run(q)
         torch.cuda.synchronize()
@@ -372,7 +375,7 @@ def run_aqr(args):
             best_vb, best_ms = vb, ms
     if rank == 0 and len(args.vbits) > 1:
         log(f"[bench] visited_bits sweep {vb_results} -> {best_vb}")
-    p = aqr.make_params(k, **m, visited_bits=best_vb, traversal=args.traversal)
+    p = aqr.make_params(k, **m, visited_bits=best_vb, traversal=args.kt)
     s = aqr.Searcher(ix, len(q), p)
     # counters for the roofline (separate, untimed run with the stats path)
     s.totals.zero_()
@@ -382,10 +385,10 @@ def run_aqr(args):
     oix, codes_equal, t_otrain = (None, None, 0.0)
     ratio, n_ratio = 1.0, 0
     if rank == 0 and not args.no_oracle:
-        oix, codes_equal, t_otrain = oracle_index(w, cfg, codes, g)
-        ratio, n_ratio = distinct_ratio_from_oracle(oix, w, m, k, traversal=args.traversal)
+        oix, codes_equal, t_otrain = oracle_index(w, cfg, codes, g, 0.0 if sq8 else float("nan"))
+        ratio, n_ratio = distinct_ratio_from_oracle(oix, w, m, k, traversal=args.kt)
     ratio = float(allreduce_sum([ratio if rank == 0 else 0.0], world)[0]) if world > 1 else ratio
-    bq = bytes_per_query(tot_counters, len(q), w.x.shape[1], k, ratio, args.traversal)
+    bq = bytes_per_query(tot_counters, len(q), w.x.shape[1], k, ratio, args.kt)
 
     # ---- device-timed region: W warm-up steps, then K steps bracketed by barrier + sync ----
     stream = torch.cuda.current_stream()
@@ -482,7 +485,7 @@ def run_aqr(args):
     # ---- CPU oracle baseline: rank 0, N = 1, bounded query sample ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and oix is not None:
-        cpu = cpu_baseline(w, oix, m, k, args.cpu_seconds, s, args.traversal)
+        cpu = cpu_baseline(w, oix, m, k, args.cpu_seconds, s, args.kt)
         cpu["codes_equal_full_size"] = codes_equal
         cpu["oracle_train_s"] = round(t_otrain, 1)
 
@@ -773,8 +776,10 @@ def main():
                     help="C5: search a rank's shards concurrently on separate CUDA streams (1) or one after another (0)")
     ap.add_argument("--stream", type=int, default=0,
                     help="also time a steady-state stream of this many fresh queries (C1/C4 under-fill the GPU)")
-    ap.add_argument("--traversal", default="aqr", choices=["aqr", "fp32"],
-                    help="aqr: the method; fp32: the paper's baseline HNSW search on the same graph (NEXT-2)")
+    ap.add_argument("--traversal", default="aqr", choices=["aqr", "fp32", "sq8"],
+                    help="aqr: the method; fp32: the paper's baseline HNSW search on the same graph; sq8: the "
+                         "paper's plain scalar-quantization HNSW (delta = 0 codes and graph, no early termination, "
+                         "full exact re-rank; R23) (NEXT-2)")
     ap.add_argument("--rerank", default="auto",
                     help="re-rank depth mappings swept: preset (Table 3, N_rerank = 28) and/or full (N_rerank = N_c); "
                          "auto = preset for C2 (identical recall there, measured), preset,full otherwise")
@@ -793,6 +798,9 @@ def main():
     if args.warmup < 3:
         log("[bench] warm-up raised to 3 (timing rule)")
         args.warmup = 3
+    args.kt = "fp32" if args.traversal == "fp32" else "aqr"  # the kernel's traversal
+    if args.traversal == "sq8":
+        args.rerank = "full"
     if args.rerank == "auto":
         args.rerank = "preset" if args.config == "C2" else "preset,full"
     if args.impl == "reference":

@@ -37,28 +37,36 @@ def _mk(name, w, delta_override=None, M=None, efc=None, p_max=5.0):
     return Case(name, w, sample, quant, codes, g, oracle.Index(w.x, codes, quant, g, w.metric), delta_override)
 
 
+def _spec(name: str):
+    if name == "tiny7":
+        return synth.gen_tiny(n=600, d=7, nq=24), dict(M=6, efc=40)
+    if name == "tiny100ip":
+        return synth.gen_tiny(n=900, d=100, nq=24, metric="ip"), dict(M=8, efc=48)
+    if name == "tiny960":
+        return synth.gen_tiny(n=300, d=960, nq=8), dict(M=8, efc=40)
+    if name == "tiny33":
+        return synth.gen_tiny(n=700, d=33, nq=24), dict(M=10, efc=50)
+    if name == "grid":
+        return synth.gen_grid(n=800, d=16, nq=24), dict(delta_override=0.0, M=8, efc=64)
+    if name == "c1":
+        return synth.gen_c1(), dict(M=None)
+    if name == "c1small":
+        return synth.gen_c1(n=3000, nq=40), dict(M=12, efc=64)
+    if name == "c2slice":
+        return synth.gen_c2(n=60_000, nq=64), dict(M=20, efc=100)
+    raise KeyError(name)
+
+
 @functools.lru_cache(maxsize=None)
 def case(name: str) -> Case:
-    if name == "tiny7":
-        return _mk(name, synth.gen_tiny(n=600, d=7, nq=24), M=6, efc=40)
-    if name == "tiny100ip":
-        return _mk(name, synth.gen_tiny(n=900, d=100, nq=24, metric="ip"), M=8, efc=48)
-    if name == "tiny960":
-        return _mk(name, synth.gen_tiny(n=300, d=960, nq=8), M=8, efc=40)
-    if name == "tiny33":
-        return _mk(name, synth.gen_tiny(n=700, d=33, nq=24), M=10, efc=50)
-    if name == "grid":
-        return _mk(name, synth.gen_grid(n=800, d=16, nq=24), delta_override=0.0, M=8, efc=64)
-    if name == "c1":
-        w = synth.gen_c1()
-        return _mk(name, w, M=None)
-    if name == "c1small":
-        w = synth.gen_c1(n=3000, nq=40)
-        return _mk(name, w, M=12, efc=64)
-    if name == "c2slice":
-        w = synth.gen_c2(n=60_000, nq=64)
-        return _mk(name, w, M=20, efc=100)
-    raise KeyError(name)
+    """`<name>_sq8`: the same workload under the plain SQ8 HNSW baseline (R23): delta = 0, so the
+    quantizer is the full-range min/max one, and the graph is built on those codes."""
+    if name.endswith("_sq8"):
+        w, kw = _spec(name[:-4])
+        kw = dict(kw, delta_override=0.0)
+    else:
+        w, kw = _spec(name)
+    return _mk(name, w, **kw)
 
 
 def near(a, b, rel=1e-5, metric="l2"):
