@@ -121,22 +121,65 @@ def bcast_np(a, world, rank, dtype):
 # clocks sampler (nvidia-smi during the timed region)
 # --------------------------------------------------------------------------------------------
 class Clocks:
+    """SM clocks and clock-event reasons sampled DURING the timed region: NVML polled from a thread
+    every 5 ms (a sample is taken at start() and at stop(), so even a ~100 ms region has samples);
+    nvidia-smi -lms 100 if NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # NVML clock-event reason bits (nvml.h)
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.p = None
+        self.nv = None
         self.lines = []
+        self.samples = []
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            uuid = str(torch.cuda.get_device_properties(self.gpu).uuid)
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+
+    def _sample(self):
+        nv, h = self.nv
+        self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                             nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM),
+                             nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+
+    def _poll(self):
+        while not self.done.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            self.done.wait(0.005)
 
     def start(self):
+        try:
+            self.nv = self._handle()
+            self._sample()
+            self.done = threading.Event()
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._rd, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5:  # the region starts once sampling runs
+                time.sleep(0.01)
         except Exception:
             self.p = None
 
@@ -145,9 +188,24 @@ class Clocks:
             self.lines.append(ln.strip())
 
     def stop(self):
+        if self.nv is not None:
+            self.done.set()
+            self.t.join(1)
+            try:
+                self._sample()
+            except Exception:
+                pass
+            sm = [float(a) for a, _, _ in self.samples]
+            mx = [float(b) for _, b, _ in self.samples]
+            reasons = {nm for _, _, r in self.samples for nm, bit in self.BITS.items() if r & bit}
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        time.sleep(0.25)
+        n0 = len(self.lines)
+        t0 = time.time()
+        while len(self.lines) == n0 and time.time() - t0 < 1:  # one sample at the region's end
+            time.sleep(0.01)
         self.p.terminate()
         try:
             self.p.wait(2)
@@ -168,7 +226,7 @@ class Clocks:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
 # --------------------------------------------------------------------------------------------
