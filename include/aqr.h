@@ -181,6 +181,9 @@ typedef struct {
   float *exact_d;       /* [nq x n_coarse] d^e of A[0:depth] */
   int64_t *counters;    /* [nq x AQR_NCOUNT] */
   int64_t *totals;      /* [AQR_NCOUNT] summed over queries (atomic adds) */
+  int64_t *t_ns;        /* [nq x 2] %globaltimer (ns) when a warp took the query and when its
+                           outputs were written: per-query latency inside a batch (Fig. 4).
+                           Timing alone (all other pointers NULL) adds no trace work. */
 } aqr_debug;
 
 /* Bytes of caller workspace aqr_search needs (device, any alignment >= 16). */

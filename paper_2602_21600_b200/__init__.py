@@ -56,7 +56,8 @@ class SearchParams(C.Structure):
 class Debug(C.Structure):
     _fields_ = [("exp_cap", C.c_int32), ("exp_ids", C.c_void_p), ("coarse_ids", C.c_void_p),
                 ("coarse_dq", C.c_void_p), ("asym_ids", C.c_void_p), ("asym_d", C.c_void_p),
-                ("exact_d", C.c_void_p), ("counters", C.c_void_p), ("totals", C.c_void_p)]
+                ("exact_d", C.c_void_p), ("counters", C.c_void_p), ("totals", C.c_void_p),
+                ("t_ns", C.c_void_p)]
 
 
 LAYOUTS = {"auto": 0, "gather": 1, "inline": 2}
@@ -275,13 +276,25 @@ class Searcher:
         self.totals = torch.zeros(NCOUNT, dtype=torch.int64, device=device)
         self._dbg = Debug()
         self._dbg.totals = self.totals.data_ptr()
+        self._tdbg = None
+        self.t_ns = None
 
-    def run(self, q, stream=None, stats=False):
+    def run(self, q, stream=None, stats=False, timing=False):
+        """timing=True: per-query [start, end] %globaltimer ns into self.t_ns [nq, 2] (no counters)."""
         torch = _torch()
         pq = _dev(q, torch.float32, "q")
+        dbg = None
+        if stats:
+            dbg = C.byref(self._dbg)
+        elif timing:
+            if self.t_ns is None or self.t_ns.shape[0] < q.shape[0]:
+                self.t_ns = torch.zeros((self.ids.shape[0], 2), dtype=torch.int64, device=self.ids.device)
+                self._tdbg = Debug()
+                self._tdbg.t_ns = self.t_ns.data_ptr()
+            dbg = C.byref(self._tdbg)
         st = lib().aqr_search(self.index.handle, pq, C.c_int64(q.shape[0]), C.c_int64(q.shape[1]),
                               C.byref(self.params), C.c_void_p(self.ids.data_ptr()),
-                              C.c_void_p(self.dist.data_ptr()), C.byref(self._dbg) if stats else None,
+                              C.c_void_p(self.dist.data_ptr()), dbg,
                               C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws.numel()), _stream(stream))
         _check(st, "aqr_search")
         return self.ids, self.dist

@@ -77,6 +77,13 @@ constexpr int kProbes = 8;
 // ------------------------------------------------------------------------------------
 // small helpers
 // ------------------------------------------------------------------------------------
+// %globaltimer: the GPU's nanosecond wall clock (per-query latency, aqr_debug.t_ns)
+__device__ __forceinline__ int64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (int64_t)t;
+}
+
 __device__ __forceinline__ uint64_t qkey(uint32_t d, int32_t id) {
   return ((uint64_t)d << 32) | ((uint64_t)(uint32_t)id << 1);
 }
@@ -872,7 +879,7 @@ __device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, c
 template <int LPR, int CPL, bool INL, int CAP, bool FP>
 __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_kernel(IndexView ix, SearchCfg c, Layout L, const float* __restrict__ q,
                                                      int64_t nq, int64_t ld_q, int32_t* __restrict__ out_ids,
-                                                     float* __restrict__ out_dist, aqr_debug dbg, int has_dbg,
+                                                     float* __restrict__ out_dist, aqr_debug dbg, int dbg_flags,
                                                      int* __restrict__ counter) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
@@ -908,11 +915,13 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     __syncwarp();
   }
 
+  const int has_dbg = dbg_flags & 1;  // trace / counters requested
   for (;;) {
     int64_t qi = 0;
     if (lane == 0) qi = atomicAdd(counter, 1);
     qi = __shfl_sync(kFull, qi, 0);
     if (qi >= nq) break;
+    if ((dbg_flags & 2) && lane == 0) dbg.t_ns[2 * qi] = globaltimer_ns();  // per-query latency
     // per-query counters live in shared memory and are only touched when a trace was requested,
     // so they cost no registers on the timed path
     int32_t* cnt = has_dbg ? scnt : nullptr;
@@ -1369,6 +1378,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
                                                        (unsigned long long)cnt[t]);
     }
     __syncwarp();
+    if ((dbg_flags & 2) && lane == 0) dbg.t_ns[2 * qi + 1] = globaltimer_ns();  // outputs written
   }
 }
 
@@ -1499,8 +1509,14 @@ cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, in
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
   aqr_debug d{};
-  if (dbg) d = *dbg;
-  kern<<<(unsigned)grid, wpb * 32, smem, s>>>(ix, cc, L, q, nq, ld_q, out_ids, out_dist, d, dbg ? 1 : 0, counter);
+  int flags = 0;
+  if (dbg) {
+    d = *dbg;
+    if (d.exp_ids || d.coarse_ids || d.coarse_dq || d.asym_ids || d.asym_d || d.exact_d || d.counters || d.totals)
+      flags |= 1;
+    if (d.t_ns) flags |= 2;
+  }
+  kern<<<(unsigned)grid, wpb * 32, smem, s>>>(ix, cc, L, q, nq, ld_q, out_ids, out_dist, d, flags, counter);
   return cudaGetLastError();
 }
 

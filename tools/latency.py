@@ -1,6 +1,8 @@
-"""Per-batch search latency on one GPU (the paper reports P50/P99 query
-latency on CPU).  One aqr_search launch per batch, CUDA events around each launch,
-batches drawn from the config's query set; prints one JSON line.
+"""Search latency on one GPU (the paper reports P50/P99 query latency on CPU,
+Fig. 4).  Per batch size: one aqr_search launch per batch with CUDA events around each
+launch (P50/P99 over reps), plus per-query latency inside one batch from the kernel's own
+%globaltimer stamps (aqr_debug.t_ns): the service time of each query on its warp and its
+completion time from the batch's first query start.  Prints one JSON line.
 
   python tools/latency.py --config C2 --ef 784 --batches 1,32,1024,10000 --reps 50
 """
@@ -52,9 +54,22 @@ def main():
             if r >= 3:
                 times.append(e0.elapsed_time(e1))
         t = np.array(times)
+        # per-query latency inside the batch (aqr_debug.t_ns, %globaltimer): service time of each
+        # query on its warp, and completion time from the batch's first query start
+        s.run(qb, timing=True)
+        torch.cuda.synchronize()
+        tn = s.t_ns[:b].cpu().numpy().astype(np.float64)
+        svc = (tn[:, 1] - tn[:, 0]) / 1e6
+        done = (tn[:, 1] - tn[:, 0].min()) / 1e6
         out["batches"].append({"batch": b, "p50_ms": round(float(np.percentile(t, 50)), 4),
                                "p99_ms": round(float(np.percentile(t, 99)), 4),
-                               "qps_p50": round(b / (np.percentile(t, 50) / 1e3), 1)})
+                               "qps_p50": round(b / (np.percentile(t, 50) / 1e3), 1),
+                               "query_service_ms": {"p50": round(float(np.percentile(svc, 50)), 4),
+                                                    "p99": round(float(np.percentile(svc, 99)), 4),
+                                                    "max": round(float(svc.max()), 4)},
+                               "query_completion_ms": {"p50": round(float(np.percentile(done, 50)), 4),
+                                                       "p99": round(float(np.percentile(done, 99)), 4),
+                                                       "max": round(float(done.max()), 4)}})
         print(json.dumps(out["batches"][-1]), file=sys.stderr, flush=True)
     print(json.dumps(out), flush=True)
 
