@@ -66,6 +66,9 @@ namespace {
 #ifndef AQR_ROWS_PER_PASS
 #define AQR_ROWS_PER_PASS 16  // 16-byte code chunks in flight per lane per gather pass
 #endif
+#ifndef AQR_LB_FIXED
+#define AQR_LB_FIXED 1  // 1: W lower bound with a warp-uniform trip count (no lane divergence)
+#endif
 #ifndef AQR_PREFETCH_ROW
 #define AQR_PREFETCH_ROW 1
 #endif
@@ -173,6 +176,13 @@ __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t 
     if (a[mid] < key) lo = mid + 1;
     else hi = mid;
   }
+  return lo;
+#elif AQR_LB_FIXED
+  // greedy bit-by-bit: the answer's bits from bit_floor(n) down; the trip count depends only on
+  // the warp-uniform n, so the lanes of a warp never diverge
+  int lo = 0;
+  for (int step = n > 0 ? 1 << (31 - __clz(n)) : 0; step > 0; step >>= 1)
+    if (lo + step <= n && a[lo + step - 1] < key) lo += step;
   return lo;
 #else
   int lo = 0, hi = n;
