@@ -841,8 +841,10 @@ def main():
     ap.add_argument("--rerank", default="auto",
                     help="re-rank depth mappings swept: preset (Table 3, N_rerank = 28) and/or full (N_rerank = N_c); "
                          "auto = preset for C2 (identical recall there, measured), preset,full otherwise")
-    ap.add_argument("--vbits", type=lambda v: [int(t) for t in v.split(",")], default=[-1],
-                    help="visited-hash sizes (log2 slots, 0 = auto) tried at the chosen ef; fastest is timed")
+    ap.add_argument("--vbits", type=lambda v: [int(t) for t in v.split(",")], default=None,
+                    help="visited-hash sizes (log2 slots; -1 = none) tried at the chosen ef, fastest is timed "
+                         "(write --vbits=-1,12). Default: -1,12,13 for C1 (100 queries leave the shared memory "
+                         "free: measured 1.8x), -1 otherwise (the hash costs occupancy: slower on C2-C4, R15)")
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -857,6 +859,8 @@ def main():
         log("[bench] warm-up raised to 3 (timing rule)")
         args.warmup = 3
     args.kt = "fp32" if args.traversal == "fp32" else "aqr"  # the kernel's traversal
+    if args.vbits is None:
+        args.vbits = [-1, 12, 13] if args.config == "C1" else [-1]
     if args.traversal == "sq8":
         args.rerank = "full"
     if args.rerank == "auto":

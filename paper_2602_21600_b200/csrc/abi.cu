@@ -315,7 +315,8 @@ aqr_status aqr_search(const aqr_index* ix, const float* q, int64_t nq, int64_t l
 #define AQR_WARPS_PER_CTA 4
 #endif
   int wpb = AQR_WARPS_PER_CTA;
-  size_t smem = aqr::search_smem_bytes(ix->v, c, wpb);
+  // one warp's state must fit a CTA (launch_search packs warps per CTA as shared memory allows)
+  size_t smem = aqr::search_smem_bytes(ix->v, c, 1);
   if (smem > 227 * 1024) {
     set_error("aqr: search: per-warp shared memory exceeds 227 KB (reduce ef or visited_bits)");
     return AQR_E_UNSUPPORTED;
