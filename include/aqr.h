@@ -150,7 +150,10 @@ typedef struct {
   int32_t assemble_mode;/* 0 = fill (R10, default), 1 = union */
   int32_t visited_bits; /* GATHER layout: log2 of the per-query visited-hash slots in shared memory,
                            6..16; 0 or -1 = no visited set (default): re-encountered nodes are
-                           re-scored and dropped by the W dedupe (R15).  INLINE: ignored. */
+                           re-scored and dropped by the W dedupe (R15); -2 = exact visited bitmap
+                           in global memory (one n-bit map per warp slot, in the caller's workspace:
+                           size it with aqr_search_workspace_size), no shared memory.  Results are
+                           identical in every mode.  INLINE: ignored. */
   int32_t warps_per_block; /* reserved, must be 0 (the CTA shape is fixed at compile time) */
   int32_t traversal;    /* AQR_TRAVERSAL_AQR (0): the method (Alg2).  AQR_TRAVERSAL_FP32 (1): the
                            paper's baseline (plain HNSW search) on the same graph: greedy
@@ -186,7 +189,8 @@ typedef struct {
                            Timing alone (all other pointers NULL) adds no trace work. */
 } aqr_debug;
 
-/* Bytes of caller workspace aqr_search needs (device, any alignment >= 16). */
+/* Bytes of caller workspace aqr_search needs (device, any alignment >= 16): 256, plus, for
+ * visited_bits = -2, min(nq rounded up to 4, 64 x SMs) bitmaps of ceil(n / 128) x 16 bytes. */
 size_t aqr_search_workspace_size(const aqr_index *ix, int64_t nq, const aqr_search_params *p);
 
 /* Search nq queries q (device [nq x ld_q] fp32).  Writes out_ids (device [nq x k] int32,

@@ -257,7 +257,22 @@ void aqr_index_free(aqr_index* ix) {
 size_t aqr_index_device_bytes(const aqr_index* ix) { return ix ? ix->bytes : 0; }
 int32_t aqr_index_layout(const aqr_index* ix) { return ix ? ix->layout : 0; }
 
-size_t aqr_search_workspace_size(const aqr_index*, int64_t, const aqr_search_params*) { return 256; }
+// 256 bytes (the persistent grid's query counter) + for visited_bits = -2 one n-bit visited bitmap
+// per warp slot (at most one slot per query, and at most 64 resident warps per SM)
+static int64_t vbm_words_of(const aqr_index* ix) { return ((ix->v.n + 127) / 128) * 4; }
+static int64_t vbm_slots_of(int64_t nq) {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t cap = (int64_t)nsm * 64;
+  const int64_t s = (nq + 3) / 4 * 4;
+  return s < cap ? s : cap;
+}
+
+size_t aqr_search_workspace_size(const aqr_index* ix, int64_t nq, const aqr_search_params* p) {
+  if (!ix || !p || p->visited_bits != -2 || nq <= 0) return 256;
+  return 256 + (size_t)vbm_slots_of(nq) * (size_t)vbm_words_of(ix) * 4;
+}
 
 static aqr_status check_search_params(const aqr_search_params* p, bool need_ef) {
   AQR_CHECK_ARG(p != nullptr, "search: params null");
@@ -273,8 +288,9 @@ static aqr_status check_search_params(const aqr_search_params* p, bool need_ef) 
   AQR_CHECK_ARG(p->tau_gap >= 0.0, "search: tau_gap must be >= 0");
   AQR_CHECK_ARG(p->tau_ratio >= 1.0, "search: tau_ratio must be >= 1");
   AQR_CHECK_ARG(p->assemble_mode == 0 || p->assemble_mode == 1, "search: assemble_mode must be 0 or 1");
-  AQR_CHECK_ARG(p->visited_bits == 0 || p->visited_bits == -1 || (p->visited_bits >= 6 && p->visited_bits <= 16),
-                "search: visited_bits must be 0 (auto), -1 (no visited hash) or in [6, 16]");
+  AQR_CHECK_ARG(p->visited_bits == 0 || p->visited_bits == -1 || p->visited_bits == -2 ||
+                    (p->visited_bits >= 6 && p->visited_bits <= 16),
+                "search: visited_bits must be 0 (auto), -1 (no visited set), -2 (global bitmap) or in [6, 16]");
   AQR_CHECK_ARG(p->warps_per_block >= 0 && p->warps_per_block <= 8, "search: warps_per_block must be in [0, 8]");
   AQR_CHECK_ARG(p->traversal == AQR_TRAVERSAL_AQR || p->traversal == AQR_TRAVERSAL_FP32,
                 "search: traversal must be AQR_TRAVERSAL_AQR (0) or AQR_TRAVERSAL_FP32 (1)");
@@ -292,6 +308,9 @@ static aqr::SearchCfg make_cfg(const aqr_search_params* p) {
   c.early_term = p->early_term;
   c.assemble_mode = p->assemble_mode;
   c.hbits = p->visited_bits > 0 ? p->visited_bits : 0;
+  c.vbm = nullptr;  // visited_bits = -2: set by aqr_search from the workspace
+  c.vbm_words = 0;
+  c.vbm_slots = 0;
   c.fp32 = p->traversal == AQR_TRAVERSAL_FP32;
   c.staged = 0;  // chosen per launch by launch_search
   return c;
@@ -322,6 +341,12 @@ aqr_status aqr_search(const aqr_index* ix, const float* q, int64_t nq, int64_t l
     return AQR_E_UNSUPPORTED;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (p->visited_bits == -2) {
+    c.vbm_words = vbm_words_of(ix);
+    c.vbm_slots = (int64_t)((ws_bytes - 256) / 4 / (size_t)c.vbm_words);
+    AQR_CHECK_ARG(c.vbm_slots >= 4, "search: workspace too small for the visited bitmaps (see aqr_search_workspace_size)");
+    c.vbm = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + 256);
+  }
   AQR_CUDA(cudaMemsetAsync(ws, 0, 256, s), "search: memset");
   AQR_CUDA(aqr::launch_search(ix->v, c, q, nq, ld_q, out_ids, out_dist, debug, static_cast<int*>(ws), wpb, s),
            "search: kernel launch");

@@ -38,6 +38,9 @@ struct SearchCfg {
   int32_t hbits;          // visited hash slots = 1 << hbits
   int32_t fp32;           // 1: FP32 baseline traversal (exact distances, no quantizer / re-rank)
   int32_t staged;         // set by the launcher: wide code rows gathered through a TMA stage
+  uint32_t* vbm;          // visited_bits = -2: per-warp-slot visited bitmaps (workspace), else null
+  int64_t vbm_words;      // 32-bit words per bitmap (multiple of 4)
+  int64_t vbm_slots;      // bitmaps available (bounds the persistent grid's warps)
 };
 
 void set_error(const std::string& msg);

@@ -909,6 +909,9 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
   int32_t* scnt = reinterpret_cast<int32_t*>(wb + H::o_cnt);
   uint8_t* blkbuf = wb + L.o_h;
   uint32_t* vhash = c.hbits > 0 ? hash : nullptr;
+  // visited_bits = -2: this warp slot's bitmap in global memory (exact; no shared memory)
+  uint32_t* vbm = (!INL && c.vbm) ? c.vbm + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * c.vbm_words
+                                  : nullptr;
   const int sub = lane % LPR;
   const int nch = ix.d_pad >> 5;
   const int ef = c.ef;
@@ -1009,10 +1012,16 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         const int nh4 = (1 << c.hbits) >> 2;
         for (int t = lane; t < nh4; t += 32) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
       }
+      if (vbm) {
+        uint4* b4 = reinterpret_cast<uint4*>(vbm);
+        for (int64_t t = lane; t < (c.vbm_words >> 2); t += 32) b4[t] = make_uint4(0, 0, 0, 0);
+        __threadfence_block();
+      }
       __syncwarp();
       if (lane == 0) {
         W[0] = qkey(dcur, cur);
         if (vhash) visit_new(hash, c.hbits, cur, fails);
+        if (vbm) atomicOr(vbm + (cur >> 5), 1u << (cur & 31));
       }
     }
     __syncwarp();
@@ -1099,7 +1108,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         }
         int deg = 0;
         m = 0;
-        if (AQR_NOCOMPACT && !vhash) {
+        if (AQR_NOCOMPACT && !vhash && !vbm) {
           // the row as it is: -1 entries are skipped by the gather and the filter
           m = ix.cap0;
 #pragma unroll
@@ -1109,6 +1118,25 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
 #pragma unroll
             for (int t = 0; t < kRowRegs; ++t)
               if (32 * t < ix.cap0) deg += __popc(__ballot_sync(kFull, arow[t] >= 0));
+          }
+        } else if (vbm) {
+          // visited bitmap: every test-and-set of the row in flight at once (one L2 round trip),
+          // then the survivors (first visits) are compacted
+          uint32_t old[kRowRegs];
+#pragma unroll
+          for (int t = 0; t < kRowRegs; ++t) {
+            const int32_t u = arow[t];
+            old[t] = (32 * t < ix.cap0 && u >= 0) ? atomicOr(vbm + (u >> 5), 1u << (u & 31)) : ~0u;
+          }
+#pragma unroll
+          for (int t = 0; t < kRowRegs; ++t) {
+            if (32 * t >= ix.cap0) break;  // uniform
+            const int32_t u = arow[t];
+            deg += __popc(__ballot_sync(kFull, u >= 0));
+            const bool keep = u >= 0 && !(old[t] & (1u << (u & 31)));
+            const uint32_t mk = __ballot_sync(kFull, keep);
+            if (keep) nb[m + __popc(mk & ((1u << lane) - 1u))] = u;
+            m += __popc(mk);
           }
         } else {
 #pragma unroll
@@ -1126,7 +1154,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         __syncwarp();
         ids = nb;
         if (cnt && lane == 0) cnt[1] += deg;
-        if (cnt && lane == 0) cnt[2] += (AQR_NOCOMPACT && !vhash) ? deg : m;
+        if (cnt && lane == 0) cnt[2] += (AQR_NOCOMPACT && !vhash && !vbm) ? deg : m;
         dists(nb, m, nd);
       }
       __syncwarp();
@@ -1517,6 +1545,7 @@ cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, in
   }
 #endif
   if (want < grid) grid = want;
+  if (cc.vbm && grid * wpb > cc.vbm_slots) grid = cc.vbm_slots / wpb;  // one bitmap per warp slot
   if (grid < 1) grid = 1;
   aqr_debug d{};
   int flags = 0;
