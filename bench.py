@@ -446,6 +446,8 @@ def run_aqr(args):
         oix, codes_equal, t_otrain = oracle_index(w, cfg, codes, g, 0.0 if sq8 else float("nan"))
         ratio, n_ratio = distinct_ratio_from_oracle(oix, w, m, k, traversal=args.kt)
     ratio = float(allreduce_sum([ratio if rank == 0 else 0.0], world)[0]) if world > 1 else ratio
+    if best_vb != -1 and best_vb != 0:
+        ratio = 1.0  # a visited set: the kernel's evaluation count is already the distinct one
     bq = bytes_per_query(tot_counters, len(q), w.x.shape[1], k, ratio, args.kt)
 
     # ---- device-timed region: W warm-up steps, then K steps bracketed by barrier + sync ----
@@ -842,9 +844,9 @@ def main():
                     help="re-rank depth mappings swept: preset (Table 3, N_rerank = 28) and/or full (N_rerank = N_c); "
                          "auto = preset for C2 (identical recall there, measured), preset,full otherwise")
     ap.add_argument("--vbits", type=lambda v: [int(t) for t in v.split(",")], default=None,
-                    help="visited-hash sizes (log2 slots; -1 = none) tried at the chosen ef, fastest is timed "
-                         "(write --vbits=-1,12). Default: -1,12,13 for C1 (100 queries leave the shared memory "
-                         "free: measured 1.8x), -1 otherwise (the hash costs occupancy: slower on C2-C4, R15)")
+                    help="visited sets tried at the chosen ef, fastest is timed (write --vbits=-1,12): -1 none, "
+                         "6..16 a shared-memory hash of 2^v slots, -2 the exact global bitmap.  Default: -2,-1,13 "
+                         "for C1, -2,-1 for C4 (re-evaluations dominate there), -1 otherwise (R15)")
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -860,7 +862,9 @@ def main():
         args.warmup = 3
     args.kt = "fp32" if args.traversal == "fp32" else "aqr"  # the kernel's traversal
     if args.vbits is None:
-        args.vbits = [-1, 12, 13] if args.config == "C1" else [-1]
+        # the exact global visited bitmap (-2) pays where re-evaluations dominate (distinct ratio
+        # 0.03 on C1, 0.09 on C4: measured 2.2x / 3.3x); elsewhere none (R15)
+        args.vbits = {"C1": [-2, -1, 13], "C4": [-2, -1]}.get(args.config, [-1])
     if args.traversal == "sq8":
         args.rerank = "full"
     if args.rerank == "auto":
