@@ -636,7 +636,7 @@ def run_sharded(args):
         g = G.build_hnsw(codes.cpu().numpy(), M, efc, synth.level_draws(n_shard, cfg="C5", shard=s_), threads,
                          flags=BUILD_FLAGS)
         ix = aqr.upload_index(codes, x, quant, g, metric="l2", id_base=s_ * n_shard, layout=LAYOUT)
-        shards.append((x, ix, aqr.Searcher(ix, nq, aqr.make_params(k, **m))))
+        shards.append((x, ix, aqr.Searcher(ix, nq, aqr.make_params(k, **m, visited_bits=args.vbits[0]))))
         # exact ground truth of this shard (global ids), merged across shards below
         gi, gd = E.ground_truth(x, q, k)
         gt_i_parts.append(gi + s_ * n_shard)
@@ -748,7 +748,7 @@ def run_sharded(args):
             "config": {"workload": f"C5: {S} shards x {n_shard} x 96 l2, {nq} queries, k={k}", "ef": m["ef"],
                        "n_coarse": m["n_coarse"], "n_rerank": m["n_rerank"], "recall@10": round(r10, 4),
                        "recall@100": round(r100, 4), "parallelism": f"{S} shards over {world} GPU(s), NCCL all-gather + merge",
-                       "shards_per_rank": len(mine), "l2": "shard indexes > 126 MB L2; no flush", "shards": infos},
+                       "shards_per_rank": len(mine), "visited_bits": args.vbits[0], "l2": "shard indexes > 126 MB L2; no flush", "shards": infos},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None, "bytes_per_query": round(bq_tot, 1),
                          "kernel": "search_kernel (all shards of rank 0)", "kernel_ms": round(kern_ms, 4),
