@@ -221,6 +221,26 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
     aqr_status st = cuda_fail(e, "upload: code norms");
     return fail(st);
   }
+  {
+    // Stage 2 decode: reciprocal scales, and whether one FMA correction reproduces every quotient
+    float* rs = (float*)alloc(sizeof(float) * V.d4);
+    int32_t* bad = (int32_t*)alloc(sizeof(int32_t));
+    if (!rs || !bad) {
+      set_error("aqr: upload: device allocation failed");
+      return fail(AQR_E_OOM);
+    }
+    int32_t bad_h = 1;
+    e = cudaMemsetAsync(bad, 0, sizeof(int32_t), s);
+    if (e == cudaSuccess) e = aqr::launch_decode_recip(sc, V.d4, rs, bad, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&bad_h, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      aqr_status st = cuda_fail(e, "upload: decode reciprocals");
+      return fail(st);
+    }
+    V.rscale_j = rs;
+    V.fast_div = bad_h == 0;
+  }
   V.blk = nullptr;
   V.blk_ids = round_up(4 * cap0, 16);
   V.blk_bytes = V.blk_ids + cap0 * V.d_pad;

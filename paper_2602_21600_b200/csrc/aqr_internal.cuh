@@ -19,6 +19,8 @@ struct IndexView {
   const float* base;      // [n x d4]   (d4 = round_up(d, 4), zero padded)
   const float* min_j;     // [d4]       (padding: 0)
   const float* scale_j;   // [d4]       (padding: 1)
+  const float* rscale_j;  // [d4] RN(1 / scale_j): Stage 2 divides by one FMA correction step
+  int32_t fast_div;       // 1: that step reproduces RN(x^ / scale_j) for every code (checked at upload)
   int32_t M, cap0, ld0;   // layer-0 rows: cap0 = 2M valid entries, stride ld0 (multiple of 8)
   const int32_t* adj0;    // [n x ld0]
   const int32_t* adj_up;  // [upper_rows x M]
@@ -55,6 +57,7 @@ cudaError_t launch_train_columns(const float* x, int64_t n, int32_t d, int64_t l
                                  cudaStream_t s);
 cudaError_t launch_encode(const float* x, int64_t n, int32_t d, int64_t ld_x, const float* min_j,
                           const float* scale_j, uint8_t* codes, int32_t d_pad, cudaStream_t s);
+cudaError_t launch_decode_recip(const float* scale, int32_t d4, float* rscale, int32_t* bad, cudaStream_t s);
 cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                           int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter,
                           int warps_per_block, cudaStream_t s);

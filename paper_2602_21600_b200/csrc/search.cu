@@ -69,6 +69,9 @@ namespace {
 #ifndef AQR_LB_FIXED
 #define AQR_LB_FIXED 1  // 1: W lower bound with a warp-uniform trip count (no lane divergence)
 #endif
+#ifndef AQR_FASTDIV
+#define AQR_FASTDIV 1  // 1: Stage 2 decode by reciprocal + one FMA correction (exact, checked at upload)
+#endif
 #ifndef AQR_PREFETCH_ROW
 #define AQR_PREFETCH_ROW 1
 #endif
@@ -677,6 +680,12 @@ __device__ __forceinline__ float warp_sum(float a) {
   return a;
 }
 
+// a / s for a code a in [0, 255] from r = RN(1/s): one FMA correction of RN(a r)
+__device__ __forceinline__ float div_code(float a, float s, float r) {
+  const float q0 = __fmul_rn(a, r);
+  return __fmaf_rn(__fmaf_rn(-q0, s, a), r, q0);
+}
+
 // four rows at once (rows with id < 0 give 0), their loads in flight together.  Per row: lanes own
 // 4-wide chunks c = lane + 32 t, one FMA per term in increasing c, then a butterfly sum.
 // Stage 2 (EXACT = false) decodes the codes x~ = x^ / scale + min (IEEE division, Alg2 l.11);
@@ -702,11 +711,26 @@ __device__ __forceinline__ void rows4(const IndexView& ix, const float* qf, cons
       const float4 sv = __ldg(reinterpret_cast<const float4*>(ix.scale_j) + c);
       const float4 mv = __ldg(reinterpret_cast<const float4*>(ix.min_j) + c);
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        xv[r].x = __fadd_rn(__fdiv_rn((float)(w[r] & 255u), sv.x), mv.x);
-        xv[r].y = __fadd_rn(__fdiv_rn((float)((w[r] >> 8) & 255u), sv.y), mv.y);
-        xv[r].z = __fadd_rn(__fdiv_rn((float)((w[r] >> 16) & 255u), sv.z), mv.z);
-        xv[r].w = __fadd_rn(__fdiv_rn((float)(w[r] >> 24), sv.w), mv.w);
+      if (AQR_FASTDIV && ix.fast_div) {
+        // RN(a / s) as q0 = RN(a r), q = RN(q0 + RN(a - q0 s) r), r = RN(1/s) (Markstein's
+        // correction; equality with the IEEE quotient verified for all 256 codes of every dimension
+        // at upload, else the division below is used)
+        const float4 rv = __ldg(reinterpret_cast<const float4*>(ix.rscale_j) + c);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          xv[r].x = __fadd_rn(div_code((float)(w[r] & 255u), sv.x, rv.x), mv.x);
+          xv[r].y = __fadd_rn(div_code((float)((w[r] >> 8) & 255u), sv.y, rv.y), mv.y);
+          xv[r].z = __fadd_rn(div_code((float)((w[r] >> 16) & 255u), sv.z, rv.z), mv.z);
+          xv[r].w = __fadd_rn(div_code((float)(w[r] >> 24), sv.w, rv.w), mv.w);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          xv[r].x = __fadd_rn(__fdiv_rn((float)(w[r] & 255u), sv.x), mv.x);
+          xv[r].y = __fadd_rn(__fdiv_rn((float)((w[r] >> 8) & 255u), sv.y), mv.y);
+          xv[r].z = __fadd_rn(__fdiv_rn((float)((w[r] >> 16) & 255u), sv.z), mv.z);
+          xv[r].w = __fadd_rn(__fdiv_rn((float)(w[r] >> 24), sv.w), mv.w);
+        }
       }
     }
 #pragma unroll
@@ -1420,6 +1444,20 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
   }
 }
 
+// r_j = RN(1 / scale_j) and a check, for every code a in [0, 255], that div_code reproduces the
+// IEEE quotient RN(a / scale_j) bit for bit (one thread per (j, a)); any mismatch sets *bad
+__global__ void decode_recip_kernel(const float* __restrict__ scale, int32_t d4, float* __restrict__ rscale,
+                                    int32_t* bad) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)d4 * 256) return;
+  const int j = (int)(t >> 8);
+  const float a = (float)(t & 255);
+  const float s = scale[j];
+  const float r = __frcp_rn(s);
+  if ((t & 255) == 0) rscale[j] = r;
+  if (__float_as_uint(div_code(a, s, r)) != __float_as_uint(__fdiv_rn(a, s))) atomicOr(bad, 1);
+}
+
 // |x^|^2 per node (exact int32: <= 255^2 * 2048 < 2^31), one thread per code row
 __global__ void code_norms_kernel(IndexView ix, int32_t* __restrict__ out) {
   const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1632,6 +1670,12 @@ cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* 
   AQR_DISPATCH(shape_of(ix), AQR_LAUNCH)
 #undef AQR_LAUNCH
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_decode_recip(const float* scale, int32_t d4, float* rscale, int32_t* bad, cudaStream_t s) {
+  const int64_t n = (int64_t)d4 * 256;
+  decode_recip_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(scale, d4, rscale, bad);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_code_norms(const IndexView& ix, int32_t* out, cudaStream_t s) {
