@@ -182,11 +182,13 @@ def search(ix: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.0
                   asym_ids=np.full((nq, n_coarse), -1, np.int32),
                   asym_d=np.full((nq, n_coarse), np.nan, np.float32),
                   exact_d=np.full((nq, n_coarse), np.nan, np.float32),
-                  counters=np.zeros((nq, NCOUNT), np.int64))
+                  counters=np.zeros((nq, NCOUNT), np.int64),
+                  upper_end=np.full((nq, max(ix.g.max_level, 1)), -1, np.int32))
     g = tr.get
     st = lib().or_search(C.byref(ix.s), _p(q), C.c_int64(nq), C.byref(p), _p(ids), _p(dist),
                          C.c_int32(exp_cap), _p(g("exp_ids")), _p(g("coarse_ids")), _p(g("coarse_dq")),
-                         _p(g("asym_ids")), _p(g("asym_d")), _p(g("exact_d")), _p(g("counters")))
+                         _p(g("asym_ids")), _p(g("asym_d")), _p(g("exact_d")), _p(g("counters")),
+                         C.c_int32(max(ix.g.max_level, 1)), _p(g("upper_end")))
     if st:
         raise ValueError(f"or_search status {st}")
     if trace:

@@ -221,6 +221,9 @@ typedef struct {
   float *asym_d;          /* [n_coarse]  d^a of A */
   float *exact_d;         /* [n_coarse]  d^e of A[0:depth] */
   int64_t *counters;      /* [OR_NCOUNT] */
+  int32_t upper_cap;      /* entries of upper_end (>= max_level to record every layer) */
+  int32_t *upper_end;     /* [upper_cap] node where the descent leaves layer L, stored at
+                             index max_level - L (trace only: no arithmetic depends on it) */
 } or_trace;
 
 enum {
@@ -251,7 +254,8 @@ static const int32_t *nbr_row(const or_index *ix, int32_t v, int32_t layer, int3
 
 /* Greedy descent through layers max_level..1 ("greedily traverses"; R8):
  * repeat cur <- argmin over {cur} U N_L(cur) of (d^q, id) until it stops changing. */
-static int32_t greedy(const or_index *ix, const uint8_t *qc, int32_t *dcur_out, int64_t *cnt) {
+static int32_t greedy(const or_index *ix, const uint8_t *qc, int32_t *dcur_out, int64_t *cnt,
+                      or_trace *tr) {
   int32_t cur = ix->entry_point;
   int32_t dcur = dq_dist(qc, ix->codes + (int64_t)cur * ix->d_pad, ix->d);
   if (cnt) cnt[C_UPPER_EVALS] += 1;
@@ -273,6 +277,7 @@ static int32_t greedy(const or_index *ix, const uint8_t *qc, int32_t *dcur_out, 
       cur = best;
       dcur = dbest;
     }
+    if (tr && tr->upper_end && ix->max_level - L < tr->upper_cap) tr->upper_end[ix->max_level - L] = cur;
   }
   *dcur_out = dcur;
   return cur;
@@ -393,37 +398,57 @@ static float decode_elem(uint8_t c, float scale, float mn) {
   return v + mn;
 }
 
-/* d^a (Alg2 l.9): sum_j (q_j - x~_j)^2 with an FMA per term, j ascending.
- * Inner product (R12): 1 - sum_j q_j x~_j. */
-static float asym_dist(const or_index *ix, const float *q, const uint8_t *xc) {
-  float acc = 0.0f;
-  if (ix->metric == 0) {
-    for (int32_t j = 0; j < ix->d; ++j) {
-      float xt = decode_elem(xc[j], ix->scale_f[j], ix->min_f[j]);
-      float e = q[j] - xt;
-      acc = fmaf(e, e, acc);
-    }
-    return acc;
+/* The fp32 sums of Stages 2 and 3 are taken in the canonical order R(32) of SURVEY 8(c)
+ * (O11/O13, "Canonical fp32 reduction R(L)"): element j belongs to the 4-wide chunk t = j/4,
+ * chunk t to partial l = t mod 32; partial l starts at +0 and accumulates its terms with one FMA
+ * each, chunks in increasing t and elements in increasing j; then, for off = 16 .. 1,
+ * every partial becomes p[l] + p[l ^ off]; the result is p[0].  A summation order is a choice
+ * the paper leaves open (it only says "FMA"); fixing it makes the fp32 values
+ * reproducible bit for bit, so no 1-ulp difference can flip the re-rank cut, the ET test or a
+ * tie by id.  tests/test_oracle_pins.py bounds it against an fp64 sum (north_star: 1e-5). */
+static float butterfly32(float *p) {
+  float t2[32];
+  for (int32_t off = 16; off >= 1; off /= 2) {
+    for (int32_t l = 0; l < 32; ++l) t2[l] = p[l] + p[l ^ off];
+    for (int32_t l = 0; l < 32; ++l) p[l] = t2[l];
   }
-  for (int32_t j = 0; j < ix->d; ++j) {
-    float xt = decode_elem(xc[j], ix->scale_f[j], ix->min_f[j]);
-    acc = fmaf(q[j], xt, acc);
-  }
-  return 1.0f - acc;
+  return p[0];
 }
 
-/* d^e (Alg2 l.19; P:197 FMA): sum_j (q_j - x_j)^2, j ascending; IP: 1 - q.x */
-static float exact_dist(const or_index *ix, const float *q, const float *x) {
-  float acc = 0.0f;
-  if (ix->metric == 0) {
-    for (int32_t j = 0; j < ix->d; ++j) {
-      float e = q[j] - x[j];
-      acc = fmaf(e, e, acc);
+/* d^a (Alg2 l.9): sum_j (q_j - x~_j)^2, an FMA per term, order R(32).
+ * Inner product (R12): 1 - sum_j q_j x~_j. */
+static float asym_dist(const or_index *ix, const float *q, const uint8_t *xc) {
+  float p[32];
+  for (int32_t l = 0; l < 32; ++l) p[l] = 0.0f;
+  for (int32_t j = 0; j < ix->d; ++j) {
+    float xt = decode_elem(xc[j], ix->scale_f[j], ix->min_f[j]);
+    int32_t l = (j / 4) % 32;
+    if (ix->metric == 0) {
+      float e = q[j] - xt;
+      p[l] = fmaf(e, e, p[l]);
+    } else {
+      p[l] = fmaf(q[j], xt, p[l]);
     }
-    return acc;
   }
-  for (int32_t j = 0; j < ix->d; ++j) acc = fmaf(q[j], x[j], acc);
-  return 1.0f - acc;
+  float acc = butterfly32(p);
+  return ix->metric == 0 ? acc : 1.0f - acc;
+}
+
+/* d^e (Alg2 l.19; P:197 FMA): sum_j (q_j - x_j)^2 in order R(32); IP: 1 - q.x */
+static float exact_dist(const or_index *ix, const float *q, const float *x) {
+  float p[32];
+  for (int32_t l = 0; l < 32; ++l) p[l] = 0.0f;
+  for (int32_t j = 0; j < ix->d; ++j) {
+    int32_t l = (j / 4) % 32;
+    if (ix->metric == 0) {
+      float e = q[j] - x[j];
+      p[l] = fmaf(e, e, p[l]);
+    } else {
+      p[l] = fmaf(q[j], x[j], p[l]);
+    }
+  }
+  float acc = butterfly32(p);
+  return ix->metric == 0 ? acc : 1.0f - acc;
 }
 
 /* Stages 2, ET, 3 and assembly for one query given C (ids sorted by (d^q,id)).
@@ -487,7 +512,7 @@ static int search_one(const or_index *ix, const float *q, const or_params *p, ui
   or_encode(q, 1, ix->d, ix->min_f, ix->scale_f, qc, ix->d_pad);
   int32_t dep;
   int64_t *cnt = tr ? tr->counters : NULL;
-  int32_t ep = greedy(ix, qc, &dep, cnt);
+  int32_t ep = greedy(ix, qc, &dep, cnt, tr);
   memset(visited, 0, (size_t)ix->n);
   int32_t wsz = (p->beam_form == 1) ? beam_heap(ix, qc, ep, dep, p->ef, visited, W, tr)
                                     : beam_flag(ix, qc, ep, dep, p->ef, visited, W, tr);
@@ -571,6 +596,7 @@ static int search_one_fp(const or_index *ix, const float *q, const or_params *p,
       cur = best;
       dcur = dbest;
     }
+    if (tr && tr->upper_end && ix->max_level - L < tr->upper_cap) tr->upper_end[ix->max_level - L] = cur;
   }
   memset(visited, 0, (size_t)ix->n);
   int32_t size = 1, ef = p->ef, nexp = 0;
@@ -632,13 +658,14 @@ static int check_params(const or_params *p) {
   return OR_OK;
 }
 
-/* Batch entry: nq queries, outputs [nq x k]; optional traces laid out per query:
+/* Batch entry: nq queries, outputs [nq x k]; optional traces laid out per query
+ * (upper_end [nq x upper_cap]: the node where the descent leaves layer L, at max_level - L):
  *   exp_ids [nq x exp_cap], exp_n [nq], coarse_ids/coarse_dq/asym_ids/asym_d/exact_d
  *   [nq x n_coarse], counters [nq x OR_NCOUNT]. */
 int or_search(const or_index *ix, const float *q, int64_t nq, const or_params *p,
               int32_t *out_ids, float *out_d, int32_t exp_cap, int32_t *exp_ids,
               int32_t *coarse_ids, int32_t *coarse_dq, int32_t *asym_ids, float *asym_d,
-              float *exact_d, int64_t *counters) {
+              float *exact_d, int64_t *counters, int32_t upper_cap, int32_t *upper_end) {
   if (check_params(p)) return OR_EINVAL;
   uint8_t *qc = (uint8_t *)calloc((size_t)ix->d_pad, 1);
   uint8_t *visited = (uint8_t *)malloc((size_t)ix->n);
@@ -661,6 +688,8 @@ int or_search(const or_index *ix, const float *q, int64_t nq, const or_params *p
     tr.asym_d = asym_d ? asym_d + i * nc : NULL;
     tr.exact_d = exact_d ? exact_d + i * nc : NULL;
     tr.counters = counters ? counters + i * OR_NCOUNT : NULL;
+    tr.upper_cap = upper_cap;
+    tr.upper_end = upper_end ? upper_end + i * upper_cap : NULL;
     if (tr.counters) memset(tr.counters, 0, sizeof(int64_t) * OR_NCOUNT);
     if (p->traversal == 1)
       st = search_one_fp(ix, q + i * ix->d, p, visited, WF, out_ids + i * p->k, out_d + i * p->k, &tr);
