@@ -1,8 +1,10 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
 
 Bar (BASELINE.json north_star): quantized codes, int32 d^q, visit order and returned ids
-bit-exact (ties by id); fp32 re-rank distances within 1e-5 relative, ids differing only
-inside such near-ties.
+bit-exact (ties by id).  The fp32 Stage 2/3 sums are taken in the canonical order R(32) on both
+sides (R24), so A, d^a, the ET flag, the re-rank depth, d^e and the final
+distances are bit-exact too -- stricter than north_star's 1e-5 relative, which is checked
+against an fp64 sum.
 """
 import numpy as np
 import pytest
@@ -63,22 +65,28 @@ def _params(c, ef):
     return dict(k=k, **m)
 
 
-def _explained(o_ad, k, depth_or, p, o_fd, g_fd, metric):
-    """Is a final-list difference explained by an fp32 near-tie (1e-5 rel) at a decision point?"""
-    n = len(o_ad)
-    cuts = [depth_or, k]
-    for cpos in cuts:
-        if 0 < cpos < n and near(o_ad[cpos - 1], o_ad[cpos], 2e-5, metric):
-            return True
-    if n > k:  # early-termination test near its threshold
-        ak, ak1 = float(o_ad[k - 1]), float(o_ad[k])
-        gap = (ak1 - ak) / (ak + 1e-6)
-        ratio = ak1 / (ak + 1e-6)
-        if abs(gap - p["tau_gap"]) <= 1e-4 * max(1.0, abs(gap)) or abs(ratio - p["tau_ratio"]) <= 1e-4 * ratio:
-            return True
-    fd = np.concatenate([o_fd, g_fd])
-    fd = np.sort(fd[np.isfinite(fd)])
-    return bool(np.any(near(fd[1:], fd[:-1], 2e-5, metric)))
+def _bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def assert_stage23_exact(o_ids, o_d, o_tr, g_ids, g_d, g_tr, ctx=""):
+    """Stages 2-3 and the output, bit for bit: both sides sum in the canonical order R(32)
+    (R24), so A (ids and d^a), the re-rank depth, the ET flag,
+    the exact d^e, the final ids and the final distances are all identical -- no tie explanation
+    is needed or allowed (ties by id, north_star)."""
+    oc, gc = o_tr["counters"], g_tr["counters"]
+    np.testing.assert_array_equal(gc[:, 6], oc[:, 6], err_msg=f"{ctx} |C|")
+    np.testing.assert_array_equal(gc[:, 7], oc[:, 7], err_msg=f"{ctx} re-rank depth")
+    np.testing.assert_array_equal(gc[:, 8], oc[:, 8], err_msg=f"{ctx} early-termination flag")
+    for i in range(len(o_ids)):
+        nc, depth = int(oc[i, 6]), int(oc[i, 7])
+        np.testing.assert_array_equal(g_tr["asym_ids"][i, :nc], o_tr["asym_ids"][i, :nc], err_msg=f"{ctx} A ids q{i}")
+        np.testing.assert_array_equal(_bits(g_tr["asym_d"][i, :nc]), _bits(o_tr["asym_d"][i, :nc]),
+                                      err_msg=f"{ctx} d^a q{i}")
+        np.testing.assert_array_equal(_bits(g_tr["exact_d"][i, :depth]), _bits(o_tr["exact_d"][i, :depth]),
+                                      err_msg=f"{ctx} d^e q{i}")
+    np.testing.assert_array_equal(g_ids, o_ids, err_msg=f"{ctx} final ids")
+    np.testing.assert_array_equal(_bits(g_d), _bits(o_d), err_msg=f"{ctx} final distances")
 
 
 @pytest.mark.parametrize("layout", ["gather", "inline"])
@@ -105,25 +113,45 @@ def test_search_parity(gpu_index, name, ef, layout):
     np.testing.assert_array_equal(g_tr["exp_ids"], o_tr["exp_ids"], err_msg="visit order")
     np.testing.assert_array_equal(g_tr["coarse_ids"], o_tr["coarse_ids"], err_msg="C ids")
     np.testing.assert_array_equal(g_tr["coarse_dq"], o_tr["coarse_dq"], err_msg="C d^q")
-    # upper-layer greedy path is identical too
-    np.testing.assert_array_equal(gc[:, 3], oc[:, 3])
-    # Stage 2: A is a permutation of C; d^a within 1e-5 relative per id
-    n_bad = 0
-    for i in range(len(q)):
-        nc = int(oc[i, 6])
-        o_map = dict(zip(o_tr["asym_ids"][i, :nc], o_tr["asym_d"][i, :nc]))
-        g_map = dict(zip(g_tr["asym_ids"][i, :nc], g_tr["asym_d"][i, :nc]))
-        assert set(o_map) == set(g_map)
-        for kk in o_map:
-            assert near(o_map[kk], g_map[kk], metric=c.w.metric), (i, kk, o_map[kk], g_map[kk])
-        # final ids exact unless explained by a near-tie
-        if not np.array_equal(o_ids[i], g_ids[i]):
-            n_bad += 1
-            assert _explained(o_tr["asym_d"][i, :nc], p["k"], int(oc[i, 7]), p, o_d[i], g_d[i], c.w.metric), (i, o_ids[i], g_ids[i])
+    # upper-layer greedy path: same row scans, neighbours and evaluations
+    np.testing.assert_array_equal(gc[:, 3:6], oc[:, 3:6], err_msg="upper-layer counters")
+    # Stages 2-3, ET, assembly: bit-exact
+    assert_stage23_exact(o_ids, o_d, o_tr, g_ids, g_d, g_tr, f"{name} ef{ef} {layout}")
+    # the north-star fp32 floor, against the oracle's fp64 sum: d^e within 1e-5 relative
+    fin = np.isfinite(o_d)
+    assert np.all(near(o_d[fin], _exact64(c, q, o_ids)[fin], metric=c.w.metric))
+
+
+def _exact64(c, q, ids):
+    x = c.w.x.astype(np.float64)
+    out = np.full(ids.shape, np.nan)
+    for i in range(len(ids)):
+        v = ids[i][ids[i] >= 0]
+        if c.w.metric == "l2":
+            out[i, :len(v)] = ((x[v] - q[i].astype(np.float64)) ** 2).sum(-1)
         else:
-            fin = np.isfinite(o_d[i])
-            assert np.all(near(o_d[i][fin], g_d[i][fin], metric=c.w.metric)), (i, o_d[i], g_d[i])
-    assert n_bad <= max(1, len(q) // 20)
+            out[i, :len(v)] = 1.0 - x[v] @ q[i].astype(np.float64)
+    return out
+
+
+@pytest.mark.parametrize("name", ["tiny33", "c1small", "tiny100ip"])
+def test_union_assembly_parity(gpu_index, name):
+    """assemble_mode = 1 (SPEC's union reading of Alg2 l.23; R10) is bit-exact too."""
+    torch = _torch()
+    aqr = _aqr()
+    c, codes, quant, ix, _ = gpu_index(name)
+    p = _params(c, 96)
+    p.update(n_rerank=p["k"], assemble_mode=1)
+    o_ids, o_d, o_tr = oracle.search(c.ix, c.w.q, trace=True, **p)
+    g_ids, g_d, g_tr = aqr.search(ix, torch.from_numpy(c.w.q).cuda(), trace=True, **p)
+    torch.cuda.synchronize()
+    g_tr = {k: v.cpu().numpy() for k, v in g_tr.items()}
+    assert_stage23_exact(o_ids, o_d, o_tr, g_ids.cpu().numpy(), g_d.cpu().numpy(), g_tr, f"{name} union")
+    # on the L2 fixtures the union reading differs from the fill reading somewhere (else the test
+    # would not test it); on tiny100ip the two coincide (measured with the oracle)
+    if c.w.metric == "l2":
+        f_ids, _ = oracle.search(c.ix, c.w.q, **dict(p, assemble_mode=0))
+        assert not np.array_equal(f_ids, o_ids)
 
 
 @pytest.mark.parametrize("name", ["tiny7", "c1small"])
@@ -138,9 +166,10 @@ def test_rerank_split_equals_fused(gpu_index, name):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(ids.cpu().numpy(), ids2.cpu().numpy())
     np.testing.assert_array_equal(d.cpu().numpy().view(np.uint32), d2.cpu().numpy().view(np.uint32))
-    # and the oracle's standalone rerank on the same C lists agrees
+    # and the oracle's standalone rerank on the same C lists is bit-identical
     o_ids, o_d = oracle.rerank(c.ix, c.w.q, tr["coarse_ids"].cpu().numpy(), p["k"], p["n_rerank"])
-    assert (o_ids == ids.cpu().numpy()).mean() > 0.97
+    np.testing.assert_array_equal(o_ids, ids.cpu().numpy())
+    np.testing.assert_array_equal(_bits(o_d), _bits(d.cpu().numpy()))
 
 
 def test_merge_topk_matches_oracle():
