@@ -66,6 +66,9 @@ namespace {
 #ifndef AQR_ROWS_PER_PASS
 #define AQR_ROWS_PER_PASS 16  // 16-byte code chunks in flight per lane per gather pass
 #endif
+#ifndef AQR_LB_SHAR
+#define AQR_LB_SHAR 1  // 1: W lower bound in Shar's form, probes unrolled (ef <= 8191)
+#endif
 #ifndef AQR_LB_FIXED
 #define AQR_LB_FIXED 1  // 1: W lower bound with a warp-uniform trip count (no lane divergence)
 #endif
@@ -74,6 +77,9 @@ namespace {
 #endif
 #ifndef AQR_PREFETCH_ROW
 #define AQR_PREFETCH_ROW 1
+#endif
+#ifndef AQR_FUSED_FILTER
+#define AQR_FUSED_FILTER 1  // 1: layer-0 scoring and the max-W filter in one pass (list_filter)
 #endif
 
 constexpr uint32_t kFull = 0xffffffffu;
@@ -180,6 +186,27 @@ __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t 
     else hi = mid;
   }
   return lo;
+#elif AQR_LB_SHAR
+  // Shar's form: after the first probe the window [i, i + k] lies inside [0, n], so the remaining
+  // probes need no bound check; they are unrolled by a switch on log2(k) (warp-uniform: n is the
+  // list size), each one LDS.64 at a constant offset from a[i] plus a 64-bit compare and add
+  if (n <= 0) return 0;
+  const int lg = 31 - __clz(n);
+  const int k = 1 << lg;
+  int i = a[k - 1] < key ? n - k : 0;
+  switch (lg) {
+#define AQR_LB_STEP(L) \
+  case L:              \
+    if (a[i + (1 << ((L)-1)) - 1] < key) i += 1 << ((L)-1);
+    AQR_LB_STEP(12) AQR_LB_STEP(11) AQR_LB_STEP(10) AQR_LB_STEP(9) AQR_LB_STEP(8) AQR_LB_STEP(7)
+    AQR_LB_STEP(6) AQR_LB_STEP(5) AQR_LB_STEP(4) AQR_LB_STEP(3) AQR_LB_STEP(2) AQR_LB_STEP(1)
+#undef AQR_LB_STEP
+    default:
+      break;
+  }
+  // the probes decide min(lb - i, k - 1); one more settles lb - i = k (a[i] is in range)
+  if (a[i] < key) ++i;
+  return i;
 #elif AQR_LB_FIXED
   // greedy bit-by-bit: the answer's bits from bit_floor(n) down; the trip count depends only on
   // the warp-uniform n, so the lanes of a warp never diverge
@@ -463,6 +490,79 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg
     for (int v = 0; v < PER; ++v) part[v] += xn[v];
     store_rows<LPR, U>(part, r0, g, sub, m, qq, out);
   }
+}
+
+// ------------------------------------------------------------------------------------
+// The layer-0 expansion's scoring and filter in one pass (AQR_FUSED_FILTER): d^q of every
+// neighbour as list_dists computes it, but instead of storing d^q and re-reading it for the
+// filter, the lane that holds a row's total forms its W key and tests it against max W at once;
+// the survivors (key < maxk, Alg2 l.7's bounded beam) are compacted into cs.  Returns their count.
+// Requirements: ids[0 .. round_up(m, pass)) readable, entries past the row's end = -1 (the
+// callers pad nb), so no row needs an `r < m` guard.  An absent row (-1) reads a stand-in row and
+// is dropped by the `id >= 0` test; a lane whose chunk lies past the row's end re-reads the last
+// chunk, multiplied by the query's zero chunk.  Same integers as list_dists.
+// ------------------------------------------------------------------------------------
+template <int LPR, int CPL>
+__device__ __forceinline__ int list_filter(const IndexView& ix, const C32 (&qreg)[CPL], int qq,
+                                           const int32_t* ids, int m, const uint64_t* W, int size, int ef,
+                                           uint64_t* cs, int lane) {
+  constexpr int G = 32 / LPR;
+  constexpr int U = rows_u<CPL>();
+  constexpr int PER = U >= LPR ? U / LPR : 1;
+  constexpr int REP = U >= LPR ? 1 : LPR / U;
+  const int g = lane / LPR, sub = lane % LPR;
+  const int nch = ix.d_pad >> 5;
+  const uint32_t dpad = (uint32_t)ix.d_pad;
+  // stand-in for absent rows: the list's first neighbour (an L2-hot row that differs from warp to
+  // warp; a fixed row would put every warp's absent rows on one L2 line -- measured, a hot spot)
+  const int alt = max(ids[0], 0);
+  int np0 = 0;
+  for (int r0 = 0; r0 < m; r0 += G * U) {
+    const int32_t* idp = ids + r0 + g * U;
+    // |x^|^2 of the rows whose totals this lane holds after the reduction
+    int xn[PER];
+#pragma unroll
+    for (int v = 0; v < PER; ++v) {
+      const int id = idp[U >= LPR ? sub * PER + v : sub / REP];
+      xn[v] = id >= 0 ? __ldg(ix.xnorm + id) : 0;
+    }
+    // an absent row (-1) reads the stand-in row `alt` instead (no predicate, no zero fill); its
+    // total is dropped by the id test below
+    C32 buf[U][CPL];
+#pragma unroll
+    for (int u4 = 0; u4 < U; u4 += 4) {
+      const int4 t4 = *reinterpret_cast<const int4*>(idp + u4);
+      const int idv[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint8_t* row = ix.codes + (uint64_t)(uint32_t)(idv[e] >= 0 ? idv[e] : alt) * dpad;
+#pragma unroll
+        for (int t = 0; t < CPL; ++t) ldg256_keep(row + 32 * min(sub + LPR * t, nch - 1), buf[u4 + e][t]);
+      }
+    }
+    int part[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      unsigned qx = 0;
+#pragma unroll
+      for (int t = 0; t < CPL; ++t) dp4a_qx(buf[u][t], qreg[t], qx);
+      part[u] = -2 * (int)qx;
+    }
+    reduce_rows<LPR, U>(part, sub);
+    // the filter against max W (W is not modified during the pass)
+    const uint64_t maxk = size >= ef ? (W[size - 1] & ~1ull) : ~0ull;
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int v = 0; v < PER; ++v) {
+      const int id = idp[U >= LPR ? sub * PER + v : sub / REP];
+      const uint64_t kk = ((uint64_t)(uint32_t)(qq + part[v] + xn[v]) << 32) | ((uint64_t)(uint32_t)id << 1);
+      const bool ok = (REP == 1 || (sub % REP) == 0) && id >= 0 && kk < maxk;
+      const uint32_t mk = __ballot_sync(kFull, ok);
+      if (ok) cs[np0 + __popc(mk & lt)] = kk;
+      np0 += __popc(mk);
+    }
+  }
+  return np0;
 }
 
 // ------------------------------------------------------------------------------------
@@ -942,6 +1042,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
   uint32_t phase = 0u;
   // wide rows: staged (TMA) gather, when the launcher chose it (c.staged)
   const bool STG = !INL && !FP && LPR == 32 && c.staged;
+  // layer-0 scoring fused with the filter (list_filter) on the GATHER layout
+  constexpr bool FUSE = !INL && !FP && AQR_FUSED_FILTER;
   uint32_t sph = 0u;                               // staged_dists parities (bit per buffer)
   if (INL || STG) {
     if (lane == 0) {
@@ -1052,7 +1154,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     // GATHER: the layer-0 row of the node to expand next is held in registers (lane owns entries
     // lane + 32 t); it is loaded for the entry point here and, afterwards, prefetched for the next
     // expansion right after the filter so the load overlaps the merge
-    constexpr int kRowRegs = 5;  // cap0 = 2M <= 160 (ABI: M <= 80)
+    constexpr int kRowRegs = (CAP + 31) / 32;  // cap0 = 2M <= CAP (56 or 160; ABI: M <= 80)
     int32_t arow[kRowRegs];
     int32_t arow2[kRowRegs];  // AQR_SPEC2: row of the guessed expansion after next
     if (!INL) {
@@ -1062,6 +1164,11 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         arow[t] = -1;
         if (32 * t < ix.cap0 && j < ix.cap0) arow[t] = __ldg(ix.adj0 + (int64_t)cur * ix.ld0 + j);
       }
+    }
+    if (FUSE) {
+      // list_filter reads whole passes of nb: entries no row fills stay -1
+      for (int i = lane; i < H::NB; i += 32) nb[i] = -1;
+      __syncwarp();
     }
     int size = 1, cursor = 0, nexp = 0;
     for (;;) {
@@ -1175,11 +1282,15 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
             m += __popc(mk);
           }
         }
+        if (FUSE && !(AQR_NOCOMPACT && !vhash && !vbm)) {
+          // list_filter reads whole passes: -1 after the compacted ids
+          for (int i = m + lane; i < (m + H::PASS - 1) / H::PASS * H::PASS; i += 32) nb[i] = -1;
+        }
         __syncwarp();
         ids = nb;
         if (cnt && lane == 0) cnt[1] += deg;
         if (cnt && lane == 0) cnt[2] += (AQR_NOCOMPACT && !vhash && !vbm) ? deg : m;
-        dists(nb, m, nd);
+        if (!(FUSE && !STG)) dists(nb, m, nd);
       }
       __syncwarp();
       // filter against max W (when full), then drop re-evaluations already in W (R15): the
@@ -1187,6 +1298,9 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       // yields each candidate's insertion rank) runs once per survivor, not once per neighbour
       const uint64_t maxk = size >= ef ? (W[size - 1] & ~1ull) : ~0ull;
       int np0 = 0;
+      if (FUSE && !STG) {
+        np0 = list_filter<LPR, CPL>(ix, qreg, qq, ids, m, W, size, ef, cs, lane);
+      } else
       for (int r0 = 0; r0 < m; r0 += 32) {
         const int r = r0 + lane;
         bool ok = false;
