@@ -36,7 +36,8 @@ namespace {
 #define AQR_WARPS_PER_CTA 4
 #endif
 #ifndef AQR_MIN_CTAS
-#define AQR_MIN_CTAS 6  // 6 CTAs x 4 warps (<= 85 regs): the shared-memory limit at ef ~ 800
+#define AQR_MIN_CTAS 6  // 6 CTAs x 4 warps (<= 80 regs).  7 (<= 72 regs; the shared memory fits at C2
+                        // ef 784 since NDA) measured 13.7 vs 10.2 ms: the register cap costs more
 #endif
 #ifndef AQR_NOCOMPACT
 #define AQR_NOCOMPACT 1  // GATHER without the visited hash: score the adjacency row as stored
@@ -77,6 +78,9 @@ namespace {
 #endif
 #ifndef AQR_PREFETCH_ROW
 #define AQR_PREFETCH_ROW 1
+#endif
+#ifndef AQR_MOVE32
+#define AQR_MOVE32 1  // 1: W segments move 32 entries per step (0: 128, four loads in flight per lane)
 #endif
 #ifndef AQR_FUSED_FILTER
 #define AQR_FUSED_FILTER 1  // 1: layer-0 scoring and the max-W filter in one pass (list_filter)
@@ -251,22 +255,32 @@ __host__ __device__ constexpr int rows_u() {
 // query aliased into the hot region (make_layout) stops short of them
 constexpr int kHotTail = 80;
 
-// the beam's per-warp scratch for adjacency rows of up to CAP entries (CAP = 56 or 160)
-template <int LPR, int CPL, int CAP>
+// the beam's per-warp scratch for adjacency rows of up to CAP entries (CAP = 56 or 160).
+// NDA (the fused list_filter path): the beam never stores d^q, so the greedy descent's d^q
+// array borrows cs and the merge's sorted insertion points (slb) borrow nb -- 4 CAP bytes less
+// per warp
+template <int LPR, int CPL, int CAP, bool NDA = false>
 struct Hot {
   static constexpr int PASS = (32 / LPR) * rows_u<CPL>();  // rows read per list_dists pass
   static constexpr int NB1 = (CAP + PASS - 1) / PASS * PASS;
   static constexpr int NB = NB1 > (CAP + 31) / 32 * 32 ? NB1 : (CAP + 31) / 32 * 32;
-  static constexpr int o_nb = 0;                            // int32 [NB] neighbour ids
-  static constexpr int o_nd = o_nb + al16(4 * NB);          // int32 [CAP] d^q
-  static constexpr int o_cand = o_nd + al16(4 * CAP);       // u64 [CAP] new W keys
-  static constexpr int o_cs = o_cand + 8 * CAP;             // u64 [CAP] survivors / sorted keys
-  static constexpr int o_lb = o_cs + 8 * CAP;               // int32 [CAP] W lower bounds
-  static constexpr int o_cnt = o_lb + al16(4 * CAP);        // int32 [16] per-query counters (debug)
-  static constexpr int o_bar = o_cnt + 64;                  // mbarriers (INLINE / staged)
-  static constexpr int bytes = o_bar + 16;                  // W follows
+  static constexpr int o_nb = 0;                                  // int32 [NB] neighbour ids
+  static constexpr int o_cand = o_nb + al16(4 * NB) + (NDA ? 0 : al16(4 * CAP));  // u64 [CAP] new W keys
+  static constexpr int o_cs = o_cand + 8 * CAP;                   // u64 [CAP] survivors / sorted keys
+  static constexpr int o_nd = NDA ? o_cs : o_nb + al16(4 * NB);   // int32 [CAP] d^q
+  static constexpr int o_slb = NDA ? o_nb : o_nd;                 // int32 [CAP] sorted insertion points
+  static constexpr int o_lb = o_cs + 8 * CAP;                     // int32 [CAP] W lower bounds
+  static constexpr int o_cnt = o_lb + al16(4 * CAP);              // int32 [16] per-query counters (debug)
+  static constexpr int o_bar = o_cnt + 64;                        // mbarriers (INLINE / staged)
+  static constexpr int bytes = o_bar + 16;                        // W follows
   static_assert(bytes - o_cnt == kHotTail, "hot tail");
 };
+
+// the Hot<> variant a kernel instantiation uses
+template <int LPR, bool INL, bool FP>
+__host__ __device__ constexpr bool nd_alias() {
+  return !INL && !FP && AQR_FUSED_FILTER && LPR < 32;
+}
 
 Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   Layout L;
@@ -1010,14 +1024,14 @@ __device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, c
 // next block prefetched during the merge) or the GATHER layout (row + per-code gathers,
 // shared-memory visited hash)
 // ------------------------------------------------------------------------------------
-template <int LPR, int CPL, bool INL, int CAP, bool FP>
+template <int LPR, int CPL, bool INL, int CAP, bool FP, bool DBG>
 __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_kernel(IndexView ix, SearchCfg c, Layout L, const float* __restrict__ q,
                                                      int64_t nq, int64_t ld_q, int32_t* __restrict__ out_ids,
                                                      float* __restrict__ out_dist, aqr_debug dbg, int dbg_flags,
                                                      int* __restrict__ counter) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
-  using H = Hot<LPR, CPL, CAP>;
+  using H = Hot<LPR, CPL, CAP, nd_alias<LPR, INL, FP>()>;
   uint8_t* wb = smem + (threadIdx.x >> 5) * L.per_warp;
   uint8_t* qc = wb + L.o_qc;
   float* qf = reinterpret_cast<float*>(wb + L.o_qf);
@@ -1054,13 +1068,14 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
     __syncwarp();
   }
 
-  const int has_dbg = dbg_flags & 1;  // trace / counters requested
+  // trace / counters requested (DBG = false: the timed instantiation, no debug code at all)
+  const int has_dbg = DBG ? (dbg_flags & 1) : 0;
   for (;;) {
     int64_t qi = 0;
     if (lane == 0) qi = atomicAdd(counter, 1);
     qi = __shfl_sync(kFull, qi, 0);
     if (qi >= nq) break;
-    if ((dbg_flags & 2) && lane == 0) dbg.t_ns[2 * qi] = globaltimer_ns();  // per-query latency
+    if (DBG && (dbg_flags & 2) && lane == 0) dbg.t_ns[2 * qi] = globaltimer_ns();  // per-query latency
     // per-query counters live in shared memory and are only touched when a trace was requested,
     // so they cost no registers on the timed path
     int32_t* cnt = has_dbg ? scnt : nullptr;
@@ -1393,7 +1408,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       // W[slb[j], slb[j+1]) (slb[np] = size), move right by j + 1 -- a constant per segment, so
       // each segment is a plain block move (top segment and top chunks first, in place; groups of
       // 4 chunks: one batch of loads, then one of stores).  Entries pushed to >= ef drop out.
-      int32_t* slb = reinterpret_cast<int32_t*>(nd);
+      int32_t* slb = reinterpret_cast<int32_t*>(wb + H::o_slb);
       for (int i = lane; i < np; i += 32) {
         const uint64_t kk = cand[i];
         int r = 0;
@@ -1476,6 +1491,22 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
           continue;
         }
 #endif
+#if AQR_MOVE32
+        // 32 entries per step, top first: one load and one store per lane.  The store of a
+        // step lands above its own loads (shift >= 1), never on entries still to be read, so
+        // one __syncwarp (loads before stores) per step suffices
+        for (; hi > seg_lo; hi -= 32) {
+          const int p = hi - 32 + lane;
+          const bool in = p >= seg_lo;
+          uint64_t v = 0;
+          if (in) v = W[p];
+          __syncwarp();
+          if (in) W[p + sh] = v;
+        }
+        __syncwarp();
+        seg_hi = seg_lo;
+        continue;
+#endif
         for (; hi > seg_lo; hi -= 128) {
           const int lo = hi - 128 > seg_lo ? hi - 128 : seg_lo;
           uint64_t v[4];
@@ -1554,7 +1585,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
                                                        (unsigned long long)cnt[t]);
     }
     __syncwarp();
-    if ((dbg_flags & 2) && lane == 0) dbg.t_ns[2 * qi + 1] = globaltimer_ns();  // outputs written
+    if (DBG && (dbg_flags & 2) && lane == 0) dbg.t_ns[2 * qi + 1] = globaltimer_ns();  // outputs written
   }
 }
 
@@ -1641,7 +1672,18 @@ template <int LPR, int CPL, bool INL, int CAP, bool FP = false>
 cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                      int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
                      cudaStream_t s) {
-  auto kern = search_kernel<LPR, CPL, INL, CAP, FP>;
+  // the flags decide before anything else: a launch without trace / counters / timestamps runs
+  // the instantiation compiled without debug code (GATHER AQR traversal; the others keep one)
+  aqr_debug d{};
+  int flags = 0;
+  if (dbg) {
+    d = *dbg;
+    if (d.exp_ids || d.coarse_ids || d.coarse_dq || d.asym_ids || d.asym_d || d.exact_d || d.counters || d.totals)
+      flags |= 1;
+    if (d.t_ns) flags |= 2;
+  }
+  auto kern = (!INL && !FP && flags == 0) ? search_kernel<LPR, CPL, INL, CAP, FP, INL || FP>
+                                          : search_kernel<LPR, CPL, INL, CAP, FP, true>;
   int dev = 0, nsm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -1654,7 +1696,7 @@ cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, in
   };
   SearchCfg cc = c;
   cc.staged = 0;
-  Layout L = make_layout(ix, cc, Hot<LPR, CPL, CAP>::bytes);
+  Layout L = make_layout(ix, cc, Hot<LPR, CPL, CAP, nd_alias<LPR, INL, FP>()>::bytes);
   if (L.per_warp > 12 * 1024) wpb = 1;  // large per-warp state: pack the SMs warp by warp
   int per_sm = 0;
   cudaError_t e = resident(L, wpb, &per_sm);
@@ -1663,7 +1705,7 @@ cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, in
     // wide code rows: stage them by TMA unless the stage costs concurrently running queries
     SearchCfg cs = c;
     cs.staged = 1;
-    const Layout Ls = make_layout(ix, cs, Hot<LPR, CPL, CAP>::bytes);
+    const Layout Ls = make_layout(ix, cs, Hot<LPR, CPL, CAP, nd_alias<LPR, INL, FP>()>::bytes);
     const int ws = Ls.per_warp > 12 * 1024 ? 1 : wpb;
     int per_sm_s = 0;
     e = resident(Ls, ws, &per_sm_s);
@@ -1699,14 +1741,6 @@ cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, in
   if (want < grid) grid = want;
   if (cc.vbm && grid * wpb > cc.vbm_slots) grid = cc.vbm_slots / wpb;  // one bitmap per warp slot
   if (grid < 1) grid = 1;
-  aqr_debug d{};
-  int flags = 0;
-  if (dbg) {
-    d = *dbg;
-    if (d.exp_ids || d.coarse_ids || d.coarse_dq || d.asym_ids || d.asym_d || d.exact_d || d.counters || d.totals)
-      flags |= 1;
-    if (d.t_ns) flags |= 2;
-  }
   kern<<<(unsigned)grid, wpb * 32, smem, s>>>(ix, cc, L, q, nq, ld_q, out_ids, out_dist, d, flags, counter);
   return cudaGetLastError();
 }
@@ -1744,7 +1778,11 @@ Shape shape_of(const IndexView& ix, bool fp = false) {
   }
 
 int hot_bytes(const IndexView& ix, bool fp) {
-#define AQR_HOT(L_, C_, K_) return Hot<L_, C_, K_>::bytes
+  const bool inl = ix.blk != nullptr;
+#define AQR_HOT(L_, C_, K_)                                                   \
+  return fp ? Hot<L_, C_, K_, nd_alias<L_, false, true>()>::bytes            \
+            : inl ? Hot<L_, C_, K_, nd_alias<L_, true, false>()>::bytes      \
+                  : Hot<L_, C_, K_, nd_alias<L_, false, false>()>::bytes
   AQR_DISPATCH(shape_of(ix, fp), AQR_HOT)
 #undef AQR_HOT
   return -1;
