@@ -54,6 +54,12 @@ def _spec(name: str):
         return synth.gen_c1(n=3000, nq=40), dict(M=12, efc=64)
     if name == "c2slice":
         return synth.gen_c2(n=60_000, nq=64), dict(M=20, efc=100)
+    # the north-star recall invariant: 200 queries, the windows bench.py uses
+    # (C2: P_max = 0.2, R4; C1: P_max = 5)
+    if name == "c2slice_nq200":
+        return synth.gen_c2(n=60_000, nq=200), dict(M=20, efc=100, p_max=0.2)
+    if name == "c1small_nq200":
+        return synth.gen_c1(n=3000, nq=200), dict(M=12, efc=64, p_max=5.0)
     raise KeyError(name)
 
 

@@ -67,15 +67,3 @@ def test_fp_equals_aqr_on_lossless_grid():
     np.testing.assert_array_equal(ta["exp_ids"], tf["exp_ids"])
     np.testing.assert_array_equal(ta["coarse_ids"], tf["coarse_ids"])
     np.testing.assert_array_equal(ta["coarse_dq"].astype(np.float32), tf["coarse_dq"].view(np.float32))
-
-
-def test_fp_search_recall_not_below_aqr_on_average():
-    """Exact traversal can only help the candidate set on average (statistical check on c1small)."""
-    c = case("c1small")
-    n = len(c.w.x)
-    gt, _ = oracle.bruteforce(c.w.x, c.w.q, 10)
-    ids_f, _ = oracle.search(c.ix, c.w.q, 10, ef=32, n_coarse=10, n_rerank=10, traversal="fp32")
-    ids_a, _ = oracle.search(c.ix, c.w.q, 10, ef=32, n_coarse=10, n_rerank=10)
-    rf = np.mean([len(set(a) & set(b)) / 10 for a, b in zip(ids_f, gt)])
-    ra = np.mean([len(set(a) & set(b)) / 10 for a, b in zip(ids_a, gt)])
-    assert rf >= ra - 0.02 and n > 0
