@@ -126,7 +126,9 @@ enum { AQR_LAYOUT_AUTO = 0, AQR_LAYOUT_GATHER = 1, AQR_LAYOUT_INLINE = 2 };
  * (code rows padded with zeros to a multiple of 32 bytes, one 256-bit load per 32 bytes, fp32 rows padded to a multiple of 4 floats, layer-0 rows padded
  * to a multiple of 8 entries).  The caller may free its inputs once the stream is
  * synchronized (this call synchronizes the stream before returning).  Validates ids,
- * entry point and sizes (AQR_E_INVALID). */
+ * entry point and sizes, and rejects a row (layer 0 or upper) that lists a neighbour twice or
+ * lists its own node (AQR_E_INVALID): the beam keeps no visited set by default (R15),
+ * so a repeated id would be scored twice in one expansion and enter W twice. */
 aqr_status aqr_upload_index(const aqr_index_desc *desc, aqr_index **out, aqr_stream_t stream);
 void aqr_index_free(aqr_index *ix);
 /* bytes of device memory owned by the index */
@@ -153,7 +155,8 @@ typedef struct {
                            re-scored and dropped by the W dedupe (R15); -2 = exact visited bitmap
                            in global memory (one n-bit map per warp slot, in the caller's workspace:
                            size it with aqr_search_workspace_size), no shared memory.  Results are
-                           identical in every mode.  INLINE: ignored. */
+                           identical in every mode.  INLINE layout (AQR traversal): only 0 / -1;
+                           -2 and 6..16 are rejected (AQR_E_INVALID): that beam keeps no visited set. */
   int32_t warps_per_block; /* reserved, must be 0 (the CTA shape is fixed at compile time) */
   int32_t traversal;    /* AQR_TRAVERSAL_AQR (0): the method (Alg2).  AQR_TRAVERSAL_FP32 (1): the
                            paper's baseline (plain HNSW search) on the same graph: greedy
@@ -215,7 +218,8 @@ aqr_status aqr_merge_topk(const float *dist, const int32_t *ids, int32_t n_lists
 
 /* Thread-local description of the last failure ("" if none). */
 const char *aqr_last_error(void);
-/* Library version string. */
+/* "aqr-b200 <version> (sm_100a) src:<16 hex digits>": the hash of the CUDA sources this
+ * library was compiled from (build.py rebuilds when it differs from the sources in the tree). */
 const char *aqr_version(void);
 
 #ifdef __cplusplus

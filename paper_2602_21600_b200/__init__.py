@@ -283,12 +283,16 @@ class Searcher:
         """timing=True: per-query [start, end] %globaltimer ns into self.t_ns [nq, 2] (no counters)."""
         torch = _torch()
         pq = _dev(q, torch.float32, "q")
+        if q.dim() != 2 or q.shape[1] != self.index.d:
+            raise AqrError(f"q must be [nq, {self.index.d}], got {tuple(q.shape)}")
+        if q.shape[0] > self.nq:
+            raise AqrError(f"batch of {q.shape[0]} queries exceeds this Searcher's {self.nq} (outputs are sized for it)")
         dbg = None
         if stats:
             dbg = C.byref(self._dbg)
         elif timing:
-            if self.t_ns is None or self.t_ns.shape[0] < q.shape[0]:
-                self.t_ns = torch.zeros((self.ids.shape[0], 2), dtype=torch.int64, device=self.ids.device)
+            if self.t_ns is None:
+                self.t_ns = torch.zeros((self.nq, 2), dtype=torch.int64, device=self.ids.device)
                 self._tdbg = Debug()
                 self._tdbg.t_ns = self.t_ns.data_ptr()
             dbg = C.byref(self._tdbg)
@@ -306,6 +310,8 @@ def search(index: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=
     """aqr_search on q [nq, d] fp32 CUDA -> (ids [nq, k] int32, dist [nq, k] fp32[, trace dict])."""
     torch = _torch()
     pq = _dev(q, torch.float32, "q")
+    if q.dim() != 2 or q.shape[1] != index.d:
+        raise AqrError(f"q must be [nq, {index.d}], got {tuple(q.shape)}")
     nq = q.shape[0]
     p = make_params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, visited_bits,
                     warps_per_block, traversal)

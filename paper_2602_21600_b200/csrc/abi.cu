@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "aqr_internal.cuh"
@@ -51,7 +52,11 @@ int32_t round_up(int32_t x, int32_t m) { return (x + m - 1) / m * m; }
 extern "C" {
 
 const char* aqr_last_error(void) { return aqr::g_err.c_str(); }
-const char* aqr_version(void) { return "aqr-b200 0.1 (sm_100a)"; }
+#ifndef AQR_SRC_HASH
+#define AQR_SRC_HASH "unknown"
+#endif
+// the build stamps the hash of the sources (paper_2602_21600_b200/build.py: src_hash)
+const char* aqr_version(void) { return "aqr-b200 0.2 (sm_100a) src:" AQR_SRC_HASH; }
 
 aqr_status aqr_encode(const float* x, int64_t n, int32_t d, int64_t ld_x, const aqr_train_cfg* train,
                       aqr_quant_params* qp, uint8_t* codes, aqr_stream_t stream) {
@@ -134,16 +139,41 @@ aqr_status aqr_upload_index(const aqr_index_desc* desc, aqr_index** out, aqr_str
   AQR_CHECK_ARG(D.layout >= AQR_LAYOUT_AUTO && D.layout <= AQR_LAYOUT_INLINE, "upload: bad layout");
   const int64_t n = D.n;
   const int32_t cap0 = 2 * D.M, M = D.M;
-  // host-side validation of the graph
-  for (int64_t i = 0; i < n * cap0; ++i)
-    AQR_CHECK_ARG(D.adj0[i] >= -1 && D.adj0[i] < n, "upload: adj0 id out of range");
+  // host-side validation of the graph: ids in range, and no row lists a node twice or lists its
+  // own node (a repeated id would be scored twice in one expansion and, having no visited set,
+  // the kernel would insert both copies into W; the oracle's visited set would not)
+  std::vector<int64_t> seen((size_t)n, -1);  // row stamp per node id
+  for (int64_t v = 0; v < n; ++v) {
+    for (int32_t t = 0; t < cap0; ++t) {
+      const int32_t u = D.adj0[v * cap0 + t];
+      AQR_CHECK_ARG(u >= -1 && u < n, "upload: adj0 id out of range");
+      if (u < 0) continue;
+      AQR_CHECK_ARG(u != v, "upload: adj0 row lists its own node (self-loop)");
+      AQR_CHECK_ARG(seen[u] != v, "upload: adj0 row lists a neighbour twice");
+      seen[u] = v;
+    }
+  }
   std::vector<int32_t> up_off((size_t)n);
+  std::vector<int64_t> owner((size_t)(D.upper_rows > 0 ? D.upper_rows : 0), -1);
   for (int64_t v = 0; v < n; ++v) {
     AQR_CHECK_ARG(D.upper_off[v] >= -1 && D.upper_off[v] < D.upper_rows, "upload: upper_off out of range");
     up_off[v] = (int32_t)D.upper_off[v];
+    if (D.upper_off[v] >= 0) owner[(size_t)D.upper_off[v]] = v;
   }
-  for (int64_t i = 0; i < D.upper_rows * M; ++i)
-    AQR_CHECK_ARG(D.adj_upper[i] >= -1 && D.adj_upper[i] < n, "upload: adj_upper id out of range");
+  // rows of a node are consecutive: a row without an owner of its own belongs to the one above
+  for (int64_t r = 1; r < D.upper_rows; ++r)
+    if (owner[(size_t)r] < 0) owner[(size_t)r] = owner[(size_t)r - 1];
+  std::fill(seen.begin(), seen.end(), -1);
+  for (int64_t r = 0; r < D.upper_rows; ++r) {
+    for (int32_t t = 0; t < M; ++t) {
+      const int32_t u = D.adj_upper[r * M + t];
+      AQR_CHECK_ARG(u >= -1 && u < n, "upload: adj_upper id out of range");
+      if (u < 0) continue;
+      AQR_CHECK_ARG(u != owner[(size_t)r], "upload: adj_upper row lists its own node (self-loop)");
+      AQR_CHECK_ARG(seen[u] != r, "upload: adj_upper row lists a neighbour twice");
+      seen[u] = r;
+    }
+  }
   if (D.max_level > 0) {
     AQR_CHECK_ARG(D.upper_off[D.entry_point] >= 0 && D.upper_off[D.entry_point] + D.max_level <= D.upper_rows,
                   "upload: entry point must have level max_level");
@@ -349,6 +379,11 @@ aqr_status aqr_search(const aqr_index* ix, const float* q, int64_t nq, int64_t l
   AQR_CHECK_ARG(ld_q >= ix->v.d, "search: ld_q < d");
   AQR_CHECK_ARG(ws != nullptr && ws_bytes >= 256, "search: workspace too small");
   AQR_CHECK_ARG(!debug || !debug->exp_ids || debug->exp_cap >= 1, "search: debug exp_cap < 1");
+  // the INLINE layout's beam reads each expansion's neighbours as one staged block and keeps no
+  // visited set: a requested one would be ignored (and the bitmap would still shrink the grid)
+  AQR_CHECK_ARG(!(ix->layout == AQR_LAYOUT_INLINE && p->traversal == AQR_TRAVERSAL_AQR &&
+                  (p->visited_bits == -2 || p->visited_bits > 0)),
+                "search: visited sets (visited_bits -2 or 6..16) need the GATHER layout");
   aqr::SearchCfg c = make_cfg(p);
 #ifndef AQR_WARPS_PER_CTA
 #define AQR_WARPS_PER_CTA 4

@@ -156,7 +156,14 @@ struct RevLink {
 
 }  // namespace
 
+#ifndef AQR_SRC_HASH
+#define AQR_SRC_HASH "unknown"
+#endif
+
 extern "C" {
+
+// the build stamps the hash of this source (build.py: src_hash) so a stale library is rebuilt
+const char* aqr_hnsw_version(void) { return "aqr-hnsw-build src:" AQR_SRC_HASH; }
 
 // Level assignment: level_i = floor(-ln(u_i) * mL), mL = 1/ln(M), u_i in (0,1]
 // supplied by the caller (seeded); capped at 30.  Fills upper_off (rows of width M for the

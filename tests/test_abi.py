@@ -91,3 +91,55 @@ def test_product_package_never_imports_oracle():
             s = open(os.path.join(ROOT, "oracle", f)).read()
             assert not re.search(r"^\s*(import|from)\s+paper_2602_21600_b200", s, re.M), f
             assert not re.search(r'^\s*#\s*include\s*"[^"]*(csrc|aqr\.h|aqr_internal)', s, re.M), f
+
+
+def test_version_carries_the_source_hash():
+    """build.py stamps the sources' hash into the library; build() rebuilds when it differs."""
+    from paper_2602_21600_b200 import build as B
+    _, deps = B._aqr_deps()
+    digest = B.src_hash(deps, B.NVCC_FLAGS)
+    assert aqr.lib().aqr_version().decode().endswith(f"src:{digest}")
+    assert B._stamped(B.LIB_AQR, digest)
+
+
+def _desc(adj0, upper_off, adj_upper, M, max_level=0, entry=0):
+    import numpy as np
+    D = aqr.IndexDesc()
+    n = adj0.shape[0]
+    D.n, D.d, D.metric, D.id_base = n, 4, 0, 0
+    D.codes, D.d_pad, D.base, D.ld_base = 16, 16, 16, 4  # never dereferenced: validation comes first
+    D.min_j, D.scale_j = 16, 16
+    D.M, D.max_level, D.entry_point = M, max_level, entry
+    D._keep = (np.ascontiguousarray(adj0, np.int32), np.ascontiguousarray(upper_off, np.int64),
+               np.ascontiguousarray(adj_upper, np.int32))
+    D.adj0 = D._keep[0].ctypes.data
+    D.upper_off = D._keep[1].ctypes.data
+    D.adj_upper = D._keep[2].ctypes.data if adj_upper.size else None
+    D.upper_rows = adj_upper.shape[0] if adj_upper.size else 0
+    D.layout = 0
+    return D
+
+
+@pytest.mark.parametrize("case", ["dup0", "self0", "dup_up", "self_up"])
+def test_upload_rejects_repeated_and_self_neighbours(case):
+    """aqr_upload_index (include/aqr.h): a row listing a neighbour twice or its own node is an
+    argument error (AQR_E_INVALID), found on the host before any device work."""
+    import numpy as np
+    lib = aqr.lib()
+    adj0 = np.array([[1, 2, -1, -1], [0, 2, -1, -1], [0, 1, 3, -1], [2, -1, -1, -1]], np.int32)
+    upper_off = np.array([0, -1, 2, -1], np.int64)   # node 0: layers 1-2 (rows 0, 1); node 2: layer 1 (row 2)
+    adj_upper = np.array([[2, -1], [-1, -1], [0, -1]], np.int32)
+    if case == "dup0":
+        adj0[2, 3] = 1
+    elif case == "self0":
+        adj0[3, 1] = 3
+    elif case == "dup_up":
+        adj_upper[0, 1] = 2
+    elif case == "self_up":
+        adj_upper[1, 0] = 0  # row 1 is node 0's layer-2 row
+    D = _desc(adj0, upper_off, adj_upper, M=2, max_level=2, entry=0)
+    h = C.c_void_p()
+    st = lib.aqr_upload_index(C.byref(D), C.byref(h), None)
+    msg = lib.aqr_last_error().decode()
+    assert st == 1, msg
+    assert ("twice" in msg) if case.startswith("dup") else ("own node" in msg), msg
