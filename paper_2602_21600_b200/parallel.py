@@ -1,8 +1,9 @@
 """Multi-GPU plumbing of the batched search: one process per GPU, torch.distributed.
 
-* C1-C4 -- replicas.  Every rank holds the whole index; the query batch is split contiguously
-  (`query_range`) or, for weak scaling, every rank searches its own full batch.  No collective
-  on the data path; `gather_rows` collects per-rank result rows for reporting only.
+* C1-C4 -- replicas.  Every rank holds the whole index and searches distinct queries: for weak
+  scaling (the default) each rank its own block of nq (`weak_block`, world x nq queries in all),
+  for strong scaling a contiguous slice of one batch (`query_range`).  No collective on the data
+  path; `gather_rows` collects per-rank result rows for reporting only.
 * C5 -- the base is sharded S ways (BASELINE.json configs[4]); rank r holds the shards
   `shards_of_rank(S, world, r)`, each a complete AQR index whose ids are offset by the shard's
   first row (`shard_rows`, passed to aqr_upload_index as id_base).  Per rank the per-shard top-k
@@ -22,6 +23,19 @@ def query_range(nq: int, world: int, rank: int) -> tuple[int, int]:
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad world/rank")
     return rank * nq // world, (rank + 1) * nq // world
+
+
+def weak_block(nq: int, world: int, rank: int) -> tuple[str, int, int]:
+    """Weak scaling of the replicated configs (C1-C4): the job is world x nq DISTINCT queries,
+    rank r searches its own block of nq.  Rank 0's block is the config's query set (so the
+    single-GPU run is the config itself); rank r >= 1 takes rows [(r-1) nq, r nq) of the
+    config's supplementary query stream (synth stream 3).  Returns (source, lo, hi) with source
+    "config" or "stream"."""
+    if world < 1 or not 0 <= rank < world or nq < 0:
+        raise ValueError("bad world/rank/nq")
+    if rank == 0:
+        return "config", 0, nq
+    return "stream", (rank - 1) * nq, rank * nq
 
 
 def shard_rows(n_total: int, n_shards: int, s: int) -> tuple[int, int]:

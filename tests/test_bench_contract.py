@@ -33,7 +33,7 @@ def test_reference_arm_contract():
     d = _run(["--impl", "reference", "--scale", "0.005", "--steps", "2", "--warmup", "3", "--cpu-seconds", "2"], 600)
     _common(d)
     assert d["impl"] == "reference"
-    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == (os.cpu_count() or 1)
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
 
 
@@ -50,3 +50,21 @@ def test_gpu_arm_contract():
     assert d["cpu_baseline"]["ids_equal_frac"] >= 0.95
     assert d["cpu_baseline"]["codes_equal_full_size"] is True
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_ranks_gloo():
+    """bench.py --gpus 2 without torchrun relaunches itself as two processes; with
+    AQR_DIST_BACKEND=gloo both ranks share the one GPU (a functional check of the N > 1 path,
+    not a measurement).  The line reports both ranks' distinct queries (weak scaling)."""
+    env = dict(os.environ, AQR_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--scale", "0.02", "--nq", "300",
+                        "--steps", "3", "--warmup", "3", "--ef", "128", "--no-cpu"], capture_output=True, text=True,
+                       timeout=1200, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    assert d["config"]["queries_per_step"] == 600 and d["config"]["queries_per_rank"] == 300
+    assert "relaunching under torch.distributed.run" in r.stderr and "rank 1/2 backend=gloo" in r.stderr

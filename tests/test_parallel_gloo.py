@@ -101,3 +101,56 @@ def test_single_process_without_group():
     assert P.gather_rows(i) is i
     od, oi = P.all_gather_lists(d, i)
     assert od.shape == (1, 2, 3) and oi.shape == (1, 2, 3)
+
+
+def _weak_worker(rank, world, port, cfg, nq, out_dir):
+    """The replicated-index weak-scaling split of bench.py: each rank materialises its own query
+    block (P.weak_block) and the blocks are gathered back in rank order."""
+    import synth
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        src, lo, hi = P.weak_block(nq, world, rank)
+        if src == "config":
+            q = synth.gen_config(cfg, scale=0.001, nq=nq).q
+        else:
+            q = synth.gen_query_stream(cfg, hi)[lo:hi]
+        allq = P.gather_rows(torch.from_numpy(np.ascontiguousarray(q)))
+        np.save(os.path.join(out_dir, f"w{rank}.npy"), allq.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_weak_scaling_queries_are_distinct_gloo(tmp_path, world):
+    """bench.py C1-C4 over N ranks (default weak scaling): N x nq DISTINCT queries, nq per rank --
+    rank 0 the config's query set, rank r >= 1 rows [(r-1) nq, r nq) of synth stream 3 -- never
+    the same queries counted once per GPU."""
+    import synth
+    cfg, nq = "C2", 50
+    mp.spawn(_weak_worker, args=(world, _free_port(), cfg, nq, str(tmp_path)), nprocs=world, join=True)
+    want = np.concatenate([synth.gen_config(cfg, scale=0.001, nq=nq).q,
+                           synth.gen_query_stream(cfg, (world - 1) * nq)])
+    for r in range(world):
+        got = np.load(tmp_path / f"w{r}.npy")
+        np.testing.assert_array_equal(got, want)
+    assert len(np.unique(want, axis=0)) == world * nq
+
+
+def test_weak_blocks():
+    for world in [1, 2, 8]:
+        blocks = [P.weak_block(10_000, world, r) for r in range(world)]
+        assert blocks[0] == ("config", 0, 10_000)
+        assert [b[1:] for b in blocks[1:]] == [((r - 1) * 10_000, r * 10_000) for r in range(1, world)]
+
+
+def test_bench_refuses_world_mismatch(monkeypatch):
+    """--gpus N must equal WORLD_SIZE under torchrun; without torchrun, N > 1 relaunches."""
+    import argparse
+    import bench
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    assert bench.relaunch_if_needed(argparse.Namespace(gpus=4)) == 2
+    assert bench.relaunch_if_needed(argparse.Namespace(gpus=2)) is None
+    monkeypatch.delenv("WORLD_SIZE")
+    assert bench.relaunch_if_needed(argparse.Namespace(gpus=1)) is None
