@@ -6,6 +6,7 @@ from __future__ import annotations
 
 import dataclasses
 import functools
+import os
 
 import numpy as np
 
@@ -33,7 +34,8 @@ def _mk(name, w, delta_override=None, M=None, efc=None, p_max=5.0):
     codes = oracle.encode(w.x, quant)
     if M is None:
         M, efc = G.adapt_params(w.M0, w.efc0, quant.delta, 0.0)
-    g = G.build_hnsw(codes, M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg="tiny"), n_threads=4)
+    g = G.build_hnsw(codes, M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg="tiny"),
+                     n_threads=min(16, os.cpu_count() or 4))
     return Case(name, w, sample, quant, codes, g, oracle.Index(w.x, codes, quant, g, w.metric), delta_override)
 
 
@@ -60,6 +62,11 @@ def _spec(name: str):
         return synth.gen_c2(n=60_000, nq=200), dict(M=20, efc=100, p_max=0.2)
     if name == "c1small_nq200":
         return synth.gen_c1(n=3000, nq=200), dict(M=12, efc=64, p_max=5.0)
+    # C4-shaped 960-d slice with C4's adapted degree class: M = 35 -> 70-entry layer-0 rows (CAP 160),
+    # LPR 32 with the TMA-staged wide-row gather; delta fixed to the C4 value (0.9972, measured on
+    # a 5000-point sample) so the slice skips the n_s^2 x 960 density pass (pinned elsewhere)
+    if name == "c4slice":
+        return synth.gen_c4(n=30_000, nq=24), dict(M=35, efc=100, delta_override=0.99720584)
     raise KeyError(name)
 
 

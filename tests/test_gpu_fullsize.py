@@ -2,21 +2,25 @@
 layout, warps per block and visited setting, the ef bench.py reports for C2): the oracle
 trains its own quantizer and encodes every base vector (compared byte for byte with
 aqr_encode), then searches a sample of queries one by one on the same graph; the GPU's visit
-order, C (ids + integer d^q) and final ids must be bit-exact, final distances within 1e-5.
+order, C (ids + integer d^q), Stages 2-3 (A, d^a, depth, ET flag, d^e) and the final ids and
+distances must be bit-exact (canonical fp32 order R(32), R24).
 
 C1 (configs[0], 10k x 128): all 100 queries at ef = 64 (BJ).
 C2 (configs[1], 1M x 128, the bench workload): 24 sampled queries at ef = 784 (the smallest
 ef with recall@10 >= 0.98 in profiles/r01) and at ef = 64."""
+import os
+
 import numpy as np
 import pytest
 
 import oracle
 import synth
 from paper_2602_21600_b200 import graph as G
+from tests.test_gpu_parity import assert_stage23_exact
 
 pytestmark = pytest.mark.gpu
 
-P_MAX = {"C1": 5.0, "C2": 0.2}  # bench.py P_MAX (DESIGN.md R4)
+P_MAX = {"C1": 5.0, "C2": 0.2, "C4": 5.0}  # bench.py P_MAX (DESIGN.md R4)
 
 
 def _build(cfg):
@@ -39,19 +43,22 @@ def _build(cfg):
     return w, ix, oracle.Index(w.x, oc, oq, g, w.metric)
 
 
-def _check(w, ix, oix, qidx, ef):
+def _check(w, ix, oix, qidx, ef, full=False, visited_bits=0):
     import torch
     import paper_2602_21600_b200 as aqr
     m = aqr.ef_mapping(ef, w.k)
+    if full:
+        m["n_rerank"] = m["n_coarse"]
     q = np.ascontiguousarray(w.q[qidx])
     o_ids, o_d, o_tr = oracle.search(oix, q, w.k, trace=True, exp_cap=4096, **m)
-    g_ids, g_d, g_tr = aqr.search(ix, torch.from_numpy(q).cuda(), w.k, trace=True, exp_cap=4096, **m)
+    g_ids, g_d, g_tr = aqr.search(ix, torch.from_numpy(q).cuda(), w.k, trace=True, exp_cap=4096,
+                                  visited_bits=visited_bits, **m)
     torch.cuda.synchronize()
-    np.testing.assert_array_equal(g_tr["exp_ids"].cpu().numpy(), o_tr["exp_ids"])
-    np.testing.assert_array_equal(g_tr["coarse_ids"].cpu().numpy(), o_tr["coarse_ids"])
-    np.testing.assert_array_equal(g_tr["coarse_dq"].cpu().numpy(), o_tr["coarse_dq"])
-    np.testing.assert_array_equal(g_ids.cpu().numpy(), o_ids)
-    np.testing.assert_allclose(g_d.cpu().numpy(), o_d, rtol=1e-5)
+    g_tr = {kk: v.cpu().numpy() for kk, v in g_tr.items()}
+    np.testing.assert_array_equal(g_tr["exp_ids"], o_tr["exp_ids"])
+    np.testing.assert_array_equal(g_tr["coarse_ids"], o_tr["coarse_ids"])
+    np.testing.assert_array_equal(g_tr["coarse_dq"], o_tr["coarse_dq"])
+    assert_stage23_exact(o_ids, o_d, o_tr, g_ids.cpu().numpy(), g_d.cpu().numpy(), g_tr, f"{w.name} ef{ef}")
 
 
 def test_c1_full():
@@ -64,3 +71,13 @@ def test_c2_full_sampled():
     qidx = np.random.default_rng(11).choice(len(w.q), 24, replace=False)
     _check(w, ix, oix, qidx, 784)
     _check(w, ix, oix, qidx, 64)
+
+
+@pytest.mark.skipif(not os.environ.get("AQR_FULL_C4"), reason="~10 min (1M x 960 host graph build); AQR_FULL_C4=1")
+def test_c4_full_sampled():
+    """BASELINE configs[3] at full size (1M x 960, M adapted to 70): the bench's point, ef 1536 with a
+    full re-rank and the exact global bitmap (visited_bits -2), 12 sampled queries.  Run on demand
+    (profiles/r02/gputest_c4_full.log): the host graph build alone takes ~7 min on the box."""
+    w, ix, oix = _build("C4")
+    qidx = np.random.default_rng(17).choice(len(w.q), 12, replace=False)
+    _check(w, ix, oix, qidx, 1536, full=True, visited_bits=-2)
