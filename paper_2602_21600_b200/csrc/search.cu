@@ -290,7 +290,9 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   // borrows the beam's scratch (AQR traversal; the fp32 baseline reads it throughout)
   const int qbytes = al16(4 * ix.d4) + al16(ix.d_pad);
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
-  L.region = ix.blk ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
+  // INLINE block buffer (AQR traversal on an INLINE index), else the visited hash.  The FP32
+  // traversal runs the GATHER kernel even on an INLINE index, so it needs the hash region
+  L.region = (ix.blk && !c.fp32) ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
   if (c.staged) {  // staged_dists: 2 x kStage wide rows
     const int st = 2 * kStage * ix.d_pad;
     if (st > L.region) L.region = st;

@@ -97,3 +97,21 @@ def test_c3_full_size_sampled():
     p = dict(k=w.k, **oracle.ef_mapping(1536, w.k))
     p["n_rerank"] = p["n_coarse"]
     _parity(oix, ix, w.q[qidx], p, -1, "C3 full ef1536")
+
+
+@pytest.mark.parametrize("vb", [-1, 12, -2])
+def test_fp32_traversal_on_inline_index(vb):
+    """The FP32-HNSW baseline (R22) runs the GATHER kernel even on an INLINE index; with the visited
+    hash its shared memory must hold the hash, not the INLINE block (found by tools/sanitize_run.py:
+    an illegal address before the fix).  Bit-exact with the oracle's fp32 mode."""
+    import torch
+    import paper_2602_21600_b200 as aqr
+    c = case("tiny33")
+    ix = _upload(c, layout="inline")
+    p = dict(k=c.w.k, **oracle.ef_mapping(48, c.w.k))
+    o_ids, o_d, o_tr = oracle.search(c.ix, c.w.q, trace=True, traversal="fp32", **p)
+    g_ids, g_d, g_tr = aqr.search(ix, torch.from_numpy(c.w.q).cuda(), trace=True, traversal="fp32", visited_bits=vb, **p)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(g_tr["exp_ids"].cpu().numpy(), o_tr["exp_ids"])
+    np.testing.assert_array_equal(g_ids.cpu().numpy(), o_ids)
+    np.testing.assert_array_equal(g_d.cpu().numpy().view(np.uint32), o_d.view(np.uint32))
