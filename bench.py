@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 EF_GRID = [16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 640, 768, 896, 1024, 1280, 1536]
 # per-config quantizer window P_max (never given by the paper; R4) and the
 # fixed HNSW construction inputs of BASELINE.json
-P_MAX = {"C1": 5.0, "C2": 0.2, "C3": 5.0, "C4": 5.0, "C5": 5.0}
+P_MAX = {"C1": 0.2, "C2": 0.2, "C3": 5.0, "C4": 0.2, "C5": 5.0}
 TARGET_RECALL = 0.98
 # the ef our arm reports (smallest ef with recall@10 >= 0.98, measured, profiles/r01): the
 # reference arm (the oracle) is timed on the same point; configs without one use BJ's ef
@@ -384,13 +384,15 @@ def run_aqr(args):
 
     def mapping(ef, mode):
         # "preset": Table 3 "0.97+" (R13); "full": the same N_c with every C entry re-ranked
-        # exactly (N_rerank = N_c) -- the Fig. 3 knob for data where d^q / d^a order is noisy (R20)
+        # exactly (N_rerank = N_c) -- the Fig. 3 knob for data where d^q / d^a order is noisy (R20);
+        # "exact": full with the early-termination thresholds at infinity (R26), so a
+        # d^a gap can no longer cut the exact re-rank to k
         mm = aqr.ef_mapping(ef, k)
         if args.traversal == "fp32":  # the baseline: W's first k are the result
             return dict(ef=max(ef, k), n_coarse=k, n_rerank=k)
-        if mode == "full" or sq8:
+        if mode in ("full", "exact") or sq8:
             mm["n_rerank"] = mm["n_coarse"]
-        if sq8:  # plain SQ8 HNSW (R23): no early termination, every C entry re-ranked exactly
+        if mode == "exact" or sq8:  # sq8: plain SQ8 HNSW (R23), every C entry re-ranked exactly
             mm["early_term"] = False
         return mm
 
@@ -936,8 +938,9 @@ def main():
                          "paper's plain scalar-quantization HNSW (delta = 0 codes and graph, no early termination, "
                          "full exact re-rank; R23) (NEXT-2)")
     ap.add_argument("--rerank", default="auto",
-                    help="re-rank depth mappings swept: preset (Table 3, N_rerank = 28) and/or full (N_rerank = N_c); "
-                         "auto = preset for C2 (identical recall there, measured), preset,full otherwise")
+                    help="re-rank mappings swept: preset (Table 3, N_rerank = 28), full (N_rerank = N_c), exact (full, "
+                         "early termination off); auto = preset for C2 (identical recall there, measured), all three "
+                         "otherwise")
     ap.add_argument("--vbits", type=lambda v: [int(t) for t in v.split(",")], default=None,
                     help="visited sets tried at the chosen ef, fastest is timed (write --vbits=-1,12): -1 none, "
                          "6..16 a shared-memory hash of 2^v slots, -2 the exact global bitmap.  Default: -2,-1,13 "
@@ -964,7 +967,7 @@ def main():
     if args.traversal == "sq8":
         args.rerank = "full"
     if args.rerank == "auto":
-        args.rerank = "preset" if args.config == "C2" else "preset,full"
+        args.rerank = "preset" if args.config == "C2" else "preset,full,exact"
     if args.impl != "reference":
         rc = relaunch_if_needed(args)
         if rc is not None:

@@ -20,7 +20,7 @@ from tests.test_gpu_parity import assert_stage23_exact
 
 pytestmark = pytest.mark.gpu
 
-P_MAX = {"C1": 5.0, "C2": 0.2, "C4": 5.0}  # bench.py P_MAX (R4)
+P_MAX = {"C1": 0.2, "C2": 0.2, "C4": 0.2}  # bench.py P_MAX (R4)
 
 
 def _build(cfg):
