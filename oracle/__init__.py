@@ -59,7 +59,8 @@ class _Index(C.Structure):
 class _Params(C.Structure):
     _fields_ = [("k", C.c_int32), ("ef", C.c_int32), ("n_coarse", C.c_int32), ("n_rerank", C.c_int32),
                 ("tau_gap", C.c_double), ("tau_ratio", C.c_double), ("early_term", C.c_int32),
-                ("assemble_mode", C.c_int32), ("beam_form", C.c_int32), ("traversal", C.c_int32)]
+                ("assemble_mode", C.c_int32), ("beam_form", C.c_int32), ("traversal", C.c_int32),
+                ("tau_spread", C.c_double)]
 
 
 def _c(a, dt):
@@ -155,8 +156,10 @@ class Index:
         self.s = s
 
 
-def _params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, beam_form, traversal=0):
+def _params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, beam_form, traversal=0,
+            tau_spread=float("inf")):
     p = _Params()
+    p.tau_spread = tau_spread
     p.traversal = {"aqr": 0, "fp32": 1}[traversal] if isinstance(traversal, str) else int(traversal)
     p.k, p.ef, p.n_coarse, p.n_rerank = k, ef, n_coarse, n_rerank
     p.tau_gap, p.tau_ratio = tau_gap, tau_ratio
@@ -165,7 +168,7 @@ def _params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_
 
 
 def search(ix: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True,
-           assemble_mode=0, beam_form=0, trace=False, exp_cap=4096, traversal="aqr"):
+           assemble_mode=0, beam_form=0, trace=False, exp_cap=4096, traversal="aqr", tau_spread=float("inf")):
     """traversal="aqr": Alg2.  traversal="fp32": the paper's baseline HNSW search
      on the same graph -- greedy + flag-form beam on exact fp32 distances in the canonical
     order R(L) (R22), result = the first k of W; coarse_dq then holds fp32 bits."""
@@ -173,7 +176,8 @@ def search(ix: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.0
     nq = q.shape[0]
     ids = np.zeros((nq, k), np.int32)
     dist = np.zeros((nq, k), np.float32)
-    p = _params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, beam_form, traversal)
+    p = _params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, beam_form, traversal,
+                tau_spread)
     tr = {}
     if trace:
         tr = dict(exp_ids=np.full((nq, exp_cap), -1, np.int32),
@@ -197,13 +201,14 @@ def search(ix: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.0
 
 
 def rerank(ix: Index, q, cand, k, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True,
-           assemble_mode=0):
+           assemble_mode=0, tau_spread=float("inf")):
     q = _c(q, np.float32)
     cand = _c(cand, np.int32)
     nq = q.shape[0]
     ids = np.zeros((nq, k), np.int32)
     dist = np.zeros((nq, k), np.float32)
-    p = _params(k, cand.shape[1], cand.shape[1], n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, 0)
+    p = _params(k, cand.shape[1], cand.shape[1], n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, 0,
+                tau_spread=tau_spread)
     st = lib().or_rerank(C.byref(ix.s), _p(q), C.c_int64(nq), _p(cand), C.c_int32(cand.shape[1]),
                          C.byref(p), _p(ids), _p(dist))
     if st:

@@ -209,6 +209,9 @@ typedef struct {
   int32_t early_term, assemble_mode; /* 0 = fill (R10), 1 = union */
   int32_t beam_form;                 /* 0 = flag form (R8), 1 = Malkov heap form */
   int32_t traversal;                 /* 0 = AQR (Alg2), 1 = FP32-HNSW baseline */
+  double tau_spread;                 /* adaptive re-rank depth (R27): +inf = the
+                                        static N_rerank; else depth = the entries of A with
+                                        d^a <= (1 + tau_spread) d^a_k, at least k, at most N_rerank */
 } or_params;
 
 /* per-query trace; any pointer may be NULL */
@@ -473,6 +476,17 @@ static int rerank_one(const or_index *ix, const float *q, const int32_t *cids, i
     term = (gap > p->tau_gap) || (ratio > p->tau_ratio);
   }
   int32_t depth = p->n_rerank < nc ? p->n_rerank : nc;
+  /* Adaptive depth ("the system evaluates the spread of asymmetric distances"; reading
+   * R27): the ambiguous band around the top-k boundary -- the entries whose d^a lies within a
+   * relative tau_spread of d^a_k (fp64 on the fp32 values) -- is re-ranked, never fewer than k */
+  if (!isinf(p->tau_spread) && nc > 0) {
+    const int32_t kk = k < nc ? k : nc;
+    const double thr = (double)A[kk - 1].v * (1.0 + p->tau_spread);
+    int32_t band = 0;
+    while (band < nc && (double)A[band].v <= thr) ++band;
+    if (band < kk) band = kk;
+    if (band < depth) depth = band;
+  }
   if (term && depth > k) depth = k;  /* "exact reranking is limited to at most k" */
   /* Stage 3: exact distances for the first `depth` entries of A (Alg2 l.19-22) */
   int32_t nr = 0;
@@ -653,7 +667,7 @@ float or_dist_fp_RL(const float *q, const float *x, int32_t d, int32_t metric) {
 
 static int check_params(const or_params *p) {
   if (p->k < 1 || p->n_coarse < p->k || p->ef < p->n_coarse || p->n_rerank < 0 ||
-      p->n_rerank > p->n_coarse || p->tau_gap < 0 || p->tau_ratio < 1)
+      p->n_rerank > p->n_coarse || p->tau_gap < 0 || p->tau_ratio < 1 || !(p->tau_spread >= 0))
     return OR_EINVAL;
   return OR_OK;
 }
