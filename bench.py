@@ -39,6 +39,7 @@ TARGET_RECALL = 0.98
 # reference arm (the oracle) is timed on the same point; configs without one use BJ's ef
 EF_AT_TARGET = {"C1": 64, "C2": 784, "C3": 1536, "C4": 128, "C5": 128}
 LAYOUT = "auto"
+WJ_LITERAL = False  # --wj literal: Alg1 l.12 as printed (NEXT-4 variant; R16)
 BUILD_FLAGS = 1  # host builder: Malkov's keepPrunedConnections (R14)
 
 
@@ -281,7 +282,7 @@ def build_index(w, cfg, rank, world, threads, delta_override=None):
     torch.cuda.synchronize()
     t_enc = time.time() - t0
     rho = quant.rho.cpu().numpy()
-    wj = G.density_weights(w.x[sample_np], rho)
+    wj = G.density_weights(w.x[sample_np], rho, literal=WJ_LITERAL)
     eta = G.eta_of(wj)
     M, efc = G.adapt_params(w.M0, w.efc0, quant.delta, eta)
     t1 = time.time()
@@ -297,7 +298,7 @@ def build_index(w, cfg, rank, world, threads, delta_override=None):
         g = G.Graph(M, efc, arrs[0], arrs[1], arrs[2], arrs[3], int(arrs[4][0]), int(arrs[4][1]))
     t_build = time.time() - t1
     ix = aqr.upload_index(codes, x, quant, g, metric=w.metric, layout=LAYOUT)
-    info = dict(layout=ix.layout, build_flags=BUILD_FLAGS, delta=quant.delta, eta=eta, M=M, efc=efc, p_max=P_MAX[cfg], p_low=quant.p_low, p_high=quant.p_high,
+    info = dict(layout=ix.layout, build_flags=BUILD_FLAGS, wj="literal" if WJ_LITERAL else "spec", delta=quant.delta, eta=eta, M=M, efc=efc, p_max=P_MAX[cfg], p_low=quant.p_low, p_high=quant.p_high,
                 encode_s=round(t_enc, 2), build_s=round(t_build, 2), max_level=g.max_level,
                 index_bytes=ix.device_bytes())
     return x, codes, quant, g, ix, info
@@ -394,6 +395,8 @@ def run_aqr(args):
             mm["n_rerank"] = mm["n_coarse"]
         if mode == "exact" or sq8:  # sq8: plain SQ8 HNSW (R23), every C entry re-ranked exactly
             mm["early_term"] = False
+        if args.tau_spread != float("inf") and not sq8:  # adaptive depth (NEXT-4, R27)
+            mm["tau_spread"] = args.tau_spread
         return mm
 
     def measure(ef, mode):
@@ -725,7 +728,7 @@ def run_sharded(args):
         samp = synth.density_sample(n_shard, cfg="C5")
         codes, quant = aqr.encode(x, sample_idx=torch.from_numpy(samp).cuda(), p_max=P_MAX["C5"], want_rho=True)
         torch.cuda.synchronize()
-        eta = G.eta_of(G.density_weights(xs[samp], quant.rho.cpu().numpy()))
+        eta = G.eta_of(G.density_weights(xs[samp], quant.rho.cpu().numpy(), literal=WJ_LITERAL))
         M, efc = G.adapt_params(32, 200, quant.delta, eta)
         g = G.build_hnsw(codes.cpu().numpy(), M, efc, synth.level_draws(n_shard, cfg="C5", shard=s_), threads,
                          flags=BUILD_FLAGS)
@@ -878,7 +881,7 @@ def run_reference(args):
     delta = oracle.delta(rho)
     quant = oracle.train(w.x, sample, p_max=P_MAX[cfg], delta_override=delta)
     codes = oracle.encode(w.x, quant)
-    eta = G.eta_of(G.density_weights(w.x[sample], rho))
+    eta = G.eta_of(G.density_weights(w.x[sample], rho, literal=WJ_LITERAL))
     M, efc = G.adapt_params(w.M0, w.efc0, quant.delta, eta)
     g = G.build_hnsw(codes, M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg=cfg), args.threads,
                      flags=BUILD_FLAGS)
@@ -953,8 +956,15 @@ def main():
                     help="C1-C4 over N GPUs: weak = N x nq distinct queries, nq per rank (default); strong = "
                          "the config's nq split across the ranks")
     ap.add_argument("--layout", default="auto", choices=["auto", "gather", "inline"])
+    ap.add_argument("--tau-spread", type=float, default=float("inf"),
+                    help="adaptive re-rank depth (P:154, R27): re-rank only the entries of A within (1 + tau) of "
+                         "d^a_k (at least k, at most N_rerank); inf = the static N_rerank (default)")
+    ap.add_argument("--wj", default="spec", choices=["spec", "literal"],
+                    help="density weights w_j for eta (builder only): spec = SPEC's per-dimension weighted "
+                         "variance (R16, default); literal = Alg1 l.12 as printed (eta = 0)")
     args = ap.parse_args()
-    global LAYOUT
+    global LAYOUT, WJ_LITERAL
+    WJ_LITERAL = args.wj == "literal"
     LAYOUT = args.layout
     if args.warmup < 3:
         log("[bench] warm-up raised to 3 (timing rule)")

@@ -164,6 +164,10 @@ typedef struct {
                            result = the first k of W; n_coarse bounds the traced C, n_rerank /
                            early_term / assemble_mode are ignored.  GATHER kernels only (an INLINE
                            index is searched through its GATHER arrays). */
+  double tau_spread;    /* adaptive re-rank depth ("evaluates the spread of asymmetric
+                           distances", R27): >= 0 re-ranks only the entries of A with
+                           d^a <= (1 + tau_spread) d^a_k (at least k, at most n_rerank); +inf
+                           (INFINITY) = the static n_rerank.  NaN or < 0: AQR_E_INVALID. */
 } aqr_search_params;
 
 enum { AQR_TRAVERSAL_AQR = 0, AQR_TRAVERSAL_FP32 = 1 };

@@ -50,7 +50,7 @@ class SearchParams(C.Structure):
     _fields_ = [("k", C.c_int32), ("ef", C.c_int32), ("n_coarse", C.c_int32), ("n_rerank", C.c_int32),
                 ("tau_gap", C.c_double), ("tau_ratio", C.c_double), ("early_term", C.c_int32),
                 ("assemble_mode", C.c_int32), ("visited_bits", C.c_int32), ("warps_per_block", C.c_int32),
-                ("traversal", C.c_int32)]
+                ("traversal", C.c_int32), ("tau_spread", C.c_double)]
 
 
 class Debug(C.Structure):
@@ -253,8 +253,9 @@ TRAVERSALS = {"aqr": 0, "fp32": 1}
 
 
 def make_params(k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True, assemble_mode=0,
-                visited_bits=0, warps_per_block=0, traversal="aqr") -> SearchParams:
+                visited_bits=0, warps_per_block=0, traversal="aqr", tau_spread=math.inf) -> SearchParams:
     p = SearchParams()
+    p.tau_spread = tau_spread
     p.traversal = TRAVERSALS[traversal]
     p.k, p.ef, p.n_coarse, p.n_rerank = k, ef, n_coarse, n_rerank
     p.tau_gap, p.tau_ratio = tau_gap, tau_ratio
@@ -306,7 +307,7 @@ class Searcher:
 
 def search(index: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True,
            assemble_mode=0, visited_bits=0, warps_per_block=0, trace=False, exp_cap=4096, stream=None,
-           traversal="aqr"):
+           traversal="aqr", tau_spread=math.inf):
     """aqr_search on q [nq, d] fp32 CUDA -> (ids [nq, k] int32, dist [nq, k] fp32[, trace dict])."""
     torch = _torch()
     pq = _dev(q, torch.float32, "q")
@@ -314,7 +315,7 @@ def search(index: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=
         raise AqrError(f"q must be [nq, {index.d}], got {tuple(q.shape)}")
     nq = q.shape[0]
     p = make_params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, visited_bits,
-                    warps_per_block, traversal)
+                    warps_per_block, traversal, tau_spread)
     dev = q.device
     ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
     dist = torch.empty((nq, k), dtype=torch.float32, device=dev)
@@ -346,13 +347,13 @@ def search(index: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=
 
 
 def rerank(index: Index, q, cand_ids, k, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True,
-           assemble_mode=0, stream=None):
+           assemble_mode=0, stream=None, tau_spread=math.inf):
     """aqr_rerank: Stages 2 / ET / 3 / assembly on cand_ids [nq, n_cand] int32 CUDA (sorted by (d^q, id))."""
     torch = _torch()
     pq = _dev(q, torch.float32, "q")
     pc = _dev(cand_ids, torch.int32, "cand_ids")
     nq, nc = cand_ids.shape
-    p = make_params(k, nc, nc, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode)
+    p = make_params(k, nc, nc, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, tau_spread=tau_spread)
     ids = torch.empty((nq, k), dtype=torch.int32, device=q.device)
     dist = torch.empty((nq, k), dtype=torch.float32, device=q.device)
     st = lib().aqr_rerank(index.handle, pq, C.c_int64(nq), C.c_int64(q.shape[1]), pc, C.c_int32(nc), C.byref(p),

@@ -337,6 +337,7 @@ static aqr_status check_search_params(const aqr_search_params* p, bool need_ef) 
   }
   AQR_CHECK_ARG(p->tau_gap >= 0.0, "search: tau_gap must be >= 0");
   AQR_CHECK_ARG(p->tau_ratio >= 1.0, "search: tau_ratio must be >= 1");
+  AQR_CHECK_ARG(p->tau_spread >= 0.0, "search: tau_spread must be >= 0 (INFINITY = static n_rerank)");
   AQR_CHECK_ARG(p->assemble_mode == 0 || p->assemble_mode == 1, "search: assemble_mode must be 0 or 1");
   AQR_CHECK_ARG(p->visited_bits == 0 || p->visited_bits == -1 || p->visited_bits == -2 ||
                     (p->visited_bits >= 6 && p->visited_bits <= 16),
@@ -355,6 +356,7 @@ static aqr::SearchCfg make_cfg(const aqr_search_params* p) {
   c.n_rerank = p->n_rerank;
   c.tau_gap = p->tau_gap;
   c.tau_ratio = p->tau_ratio;
+  c.tau_spread = p->tau_spread;
   c.early_term = p->early_term;
   c.assemble_mode = p->assemble_mode;
   c.hbits = p->visited_bits > 0 ? p->visited_bits : 0;

@@ -36,6 +36,7 @@ struct IndexView {
 struct SearchCfg {
   int32_t k, ef, n_coarse, n_rerank;
   double tau_gap, tau_ratio;
+  double tau_spread;      // adaptive re-rank depth (R27); +inf = static n_rerank
   int32_t early_term, assemble_mode;
   int32_t hbits;          // visited hash slots = 1 << hbits
   int32_t fp32;           // 1: FP32 baseline traversal (exact distances, no quantizer / re-rank)

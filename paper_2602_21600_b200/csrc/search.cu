@@ -910,6 +910,20 @@ __device__ void finish_query(const IndexView& ix, const SearchCfg& c, const floa
     term = (gap > c.tau_gap) || (ratio > c.tau_ratio);
   }
   int depth = c.n_rerank < nc ? c.n_rerank : nc;
+  if (!isinf(c.tau_spread) && nc > 0) {
+    // adaptive depth (R27): the entries of A (sorted) with d^a <= (1 + tau_spread) d^a_k,
+    // at least k, at most N_rerank -- a prefix of A, counted by ballots
+    const int kk = k < nc ? k : nc;
+    const double thr = __dmul_rn((double)fkey_inv((uint32_t)(akeys[kk - 1] >> 32)), __dadd_rn(1.0, c.tau_spread));
+    int band = 0;
+    for (int i0 = 0; i0 < nc; i0 += 32) {
+      const int i = i0 + lane;
+      const bool in = i < nc && (double)fkey_inv((uint32_t)(akeys[i] >> 32)) <= thr;
+      band += __popc(__ballot_sync(kFull, in));
+    }
+    if (band < kk) band = kk;
+    if (band < depth) depth = band;
+  }
   if (term && depth > k) depth = k;
   // Stage 3: exact distances for A[0:depth] (Alg2 l.19-22)
   for (int i0 = 0; i0 < depth; i0 += 4) {

@@ -68,11 +68,15 @@ def build_hnsw(codes: np.ndarray, M: int, efc: int, level_u: np.ndarray, n_threa
     return Graph(M, efc, levels, upper_off, adj0, adj_upper, int(out2[0]), int(out2[1]))
 
 
-def density_weights(x_sample: np.ndarray, rho: np.ndarray) -> np.ndarray:
+def density_weights(x_sample: np.ndarray, rho: np.ndarray, literal: bool = False) -> np.ndarray:
     """w_j (Alg1 l.12) -- as printed, w_j = (1/n) sum rho_i is j-independent; R16 takes
-    SPEC's density-weighted per-dimension variance, floored at 1e-12, normalised to mean 1."""
+    SPEC's density-weighted per-dimension variance, floored at 1e-12, normalised to mean 1.
+    literal=True (NEXT-4 variant): the formula as printed, the mean density for every j -- then
+    sigma_w = 0, eta = 0, M_i = floor(M0 (1 + delta)) and ef_c = ef_0 (Alg1 l.14, l.17-18)."""
     x = x_sample.astype(np.float64)
     r = rho.astype(np.float64)
+    if literal:
+        return np.full(x.shape[1], r.mean())
     mu = (r[:, None] * x).sum(0) / r.sum()
     w = (r[:, None] * (x - mu) ** 2).sum(0) / r.sum()
     w = np.maximum(w, 1e-12)
@@ -80,7 +84,9 @@ def density_weights(x_sample: np.ndarray, rho: np.ndarray) -> np.ndarray:
 
 
 def eta_of(w: np.ndarray) -> float:
-    """eta = sigma_w / w_bar (Alg1 l.14), population std."""
+    """eta = sigma_w / w_bar (Alg1 l.14), population std (exactly 0 for constant w)."""
+    if np.ptp(w) == 0:
+        return 0.0
     return float(np.sqrt(((w - w.mean()) ** 2).mean()) / w.mean())
 
 

@@ -201,3 +201,22 @@ def test_lossless_grid_equals_bruteforce(gpu_index):
     ids, d = aqr.search(ix, torch.from_numpy(c.w.q).cuda(), k=k, ef=n, n_coarse=n, n_rerank=n, early_term=False)
     bf_ids, bf_d = oracle.bruteforce(c.w.x, c.w.q, k)
     np.testing.assert_array_equal(ids.cpu().numpy(), bf_ids)
+
+
+@pytest.mark.parametrize("name", ["tiny33", "tiny100ip", "c1small", "c2slice"])
+@pytest.mark.parametrize("tau", [0.0, 0.05, 0.5])
+def test_adaptive_depth_parity(gpu_index, name, tau):
+    """Adaptive re-rank depth (NEXT-4, R27): the band of A within (1 + tau_spread) d^a_k is
+    re-ranked; depth, ET flag, d^e, ids and distances bit-exact with the oracle."""
+    torch = _torch()
+    aqr = _aqr()
+    c, codes, quant, ix, _ = gpu_index(name)
+    p = _params(c, 96)
+    p["n_rerank"] = p["n_coarse"]
+    o_ids, o_d, o_tr = oracle.search(c.ix, c.w.q, trace=True, tau_spread=tau, **p)
+    g_ids, g_d, g_tr = aqr.search(ix, torch.from_numpy(c.w.q).cuda(), trace=True, tau_spread=tau, **p)
+    torch.cuda.synchronize()
+    g_tr = {k: v.cpu().numpy() for k, v in g_tr.items()}
+    assert_stage23_exact(o_ids, o_d, o_tr, g_ids.cpu().numpy(), g_d.cpu().numpy(), g_tr, f"{name} tau {tau}")
+    if tau == 0.0:  # a narrow band really changes the depth somewhere
+        assert (o_tr["counters"][:, 7] < p["n_rerank"]).any()

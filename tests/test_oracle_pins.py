@@ -228,3 +228,17 @@ def test_table3_and_ef_mapping():
     assert m == dict(ef=165, n_coarse=55, n_rerank=28)
     m = oracle.ef_mapping(16, 10)
     assert m["n_coarse"] == 10 and m["n_rerank"] == 10 and m["ef"] == 16
+
+
+def test_literal_density_weights():
+    """NEXT-4 variant: w_j as printed in Alg1 l.12, (1/n) sum_i rho_i for every j, so
+    sigma_w = 0, eta = 0 (Alg1 l.14), M_i = floor(M0 (1 + delta)) and ef_c = ef_0 (Alg1 l.17-18)."""
+    from paper_2602_21600_b200 import graph as G
+    rng = np.random.default_rng(4)
+    x = rng.normal(size=(300, 17)).astype(np.float32)
+    rho = rng.uniform(0.1, 3.0, size=300)
+    w = G.density_weights(x, rho, literal=True)
+    assert w.shape == (17,) and np.all(w == rho.mean())
+    assert G.eta_of(w) == 0.0
+    assert G.adapt_params(16, 200, 0.5, G.eta_of(w)) == (24, 200)
+    assert G.eta_of(G.density_weights(x, rho)) > 0  # the SPEC reading (R16) varies with j
