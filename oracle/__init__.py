@@ -41,6 +41,7 @@ def lib():
         _lib = C.CDLL(build())
         _lib.or_delta.restype = C.c_double
         _lib.or_percentile_sorted.restype = C.c_double
+        _lib.or_build_upper_rows.restype = C.c_int64
     return _lib
 
 
@@ -296,3 +297,35 @@ def decode(code, scale, mn):
     L = lib()
     L.or_decode.restype = C.c_float
     return float(L.or_decode(C.c_uint8(code), C.c_float(scale), C.c_float(mn)))
+
+
+# ------------------------------------------------------------------------------------------
+# graph construction (Alg1 l.16-22; the oracle of the GPU index build, R28)
+# ------------------------------------------------------------------------------------------
+def build_levels(u, M):
+    """Node levels floor(-ln(u) / ln(M)), capped at 30, from uniform draws u in (0, 1]."""
+    u = _c(u, np.float64)
+    lv = np.zeros(len(u), np.int32)
+    lib().or_build_levels(_p(u), C.c_int64(len(u)), C.c_int32(M), _p(lv))
+    return lv
+
+
+def build_graph(codes, d, M, efc, level_u, flags=1, batch_div=32):
+    """HNSW insertion over the codes [n, d_pad] in the wave order of DESIGN.md R28 ->
+    (levels, upper_off, adj0 [n, 2M], adj_upper [rows, M], entry_point, max_level)."""
+    codes = _c(codes, np.uint8)
+    n, d_pad = codes.shape
+    levels = build_levels(level_u, M)
+    upper_off = np.zeros(n, np.int64)
+    rows = int(lib().or_build_upper_rows(_p(levels), C.c_int64(n), _p(upper_off)))
+    adj0 = np.zeros((n, 2 * M), np.int32)
+    adj_upper = np.zeros((max(rows, 1), M), np.int32)
+    em = np.zeros(2, np.int32)
+    L = lib()
+    L.or_build_upper_rows.restype = C.c_int64
+    st = L.or_build_graph(_p(codes), C.c_int64(n), C.c_int32(d), C.c_int32(d_pad), _p(levels), _p(upper_off),
+                          C.c_int32(M), C.c_int32(efc), C.c_int32(flags), C.c_int32(batch_div), _p(adj0),
+                          _p(adj_upper), _p(em))
+    if st:
+        raise ValueError(f"or_build_graph status {st}")
+    return levels, upper_off, adj0, adj_upper[:rows], int(em[0]), int(em[1])

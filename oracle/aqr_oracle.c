@@ -807,6 +807,217 @@ int or_bruteforce_dq(const uint8_t *codes, int64_t n, int32_t d, int32_t d_pad, 
   return OR_OK;
 }
 
+/* ==================================================================================== */
+/* Build phase, Stage 3: graph construction (Alg1 l.16-22) -- the ORACLE of the    */
+/* GPU index build.  HNSW insertion [23] over the quantized codes  */
+/* with d^q and (d, id) ties, in the wave order of DESIGN.md R28: nodes are inserted in id     */
+/* order in batches; every node of a batch searches the graph as it stood when the batch began */
+/* and chooses its own neighbours; then the reverse links of the batch are applied per (layer, */
+/* target row), sources in id order, pruning a full row with the same selection rule.         */
+/* ==================================================================================== */
+
+/* level of a node from its uniform draw u in (0, 1]: floor(-ln(u) / ln(M)), cap 30 */
+void or_build_levels(const double *u, int64_t n, int32_t M, int32_t *levels) {
+  for (int64_t i = 0; i < n; ++i) {
+    double lv = floor(-log(u[i]) * (1.0 / log((double)M)));
+    levels[i] = lv > 30.0 ? 30 : (int32_t)lv;
+  }
+}
+
+typedef struct {
+  const uint8_t *codes;
+  int64_t n;
+  int32_t d, d_pad, M, cap0;
+  const int32_t *levels;
+  const int64_t *upper_off;
+  int32_t *adj0, *adj_upper;
+  uint32_t *stamp;   /* visited marks of the current layer search */
+  uint32_t epoch;
+} or_bgraph;
+
+static int32_t *brow(const or_bgraph *g, int64_t v, int32_t L) {
+  return L == 0 ? g->adj0 + v * g->cap0 : g->adj_upper + (g->upper_off[v] + L - 1) * g->M;
+}
+static int32_t bdist(const or_bgraph *g, int64_t a, int64_t b) {
+  return dq_dist(g->codes + a * g->d_pad, g->codes + b * g->d_pad, g->d);
+}
+
+/* SEARCH-LAYER [23] in the flag form (R8) from several entry points (sorted by
+ * (d, id)): W starts as the ef smallest of them, all unexpanded, and all are marked visited.
+ * Rows end at their first -1.  Returns |W|; W sorted by (d, id). */
+static int32_t bsearch_layer(or_bgraph *g, int64_t q, const or_went *eps, int32_t n_eps, int32_t ef, int32_t L,
+                             or_went *W) {
+  if (++g->epoch == 0) { memset(g->stamp, 0, sizeof(uint32_t) * (size_t)g->n); g->epoch = 1; }
+  int32_t size = 0;
+  for (int32_t i = 0; i < n_eps; ++i) {
+    g->stamp[eps[i].id] = g->epoch;
+    if (size < ef) { W[size] = eps[i]; W[size].expanded = 0; ++size; }
+  }
+  const int32_t cap = L == 0 ? g->cap0 : g->M;
+  for (;;) {
+    int32_t ci = -1;
+    for (int32_t i = 0; i < size; ++i)
+      if (!W[i].expanded) { ci = i; break; }
+    if (ci < 0) break;
+    W[ci].expanded = 1;
+    const int32_t *row = brow(g, W[ci].id, L);
+    for (int32_t t = 0; t < cap; ++t) {
+      int32_t u = row[t];
+      if (u < 0) break;
+      if (g->stamp[u] == g->epoch) continue;
+      g->stamp[u] = g->epoch;
+      int32_t du = bdist(g, q, u);
+      if (size < ef || key_less(du, u, W[size - 1].d, W[size - 1].id)) {
+        int32_t pos = size < ef ? size : ef - 1;
+        while (pos > 0 && key_less(du, u, W[pos - 1].d, W[pos - 1].id)) { W[pos] = W[pos - 1]; --pos; }
+        W[pos].d = du; W[pos].id = u; W[pos].expanded = 0;
+        if (size < ef) ++size;
+      }
+    }
+  }
+  return size;
+}
+
+/* Malkov's neighbour-selection heuristic (R14): scan the candidates in (d, id) order (d = distance
+ * to the base node); keep e unless an already kept r is strictly closer to e than the base is
+ * (d(e, r) < d(e)); stop at m kept.  keep_pruned: fill the free slots with the rejected ones, in
+ * scan order.  Returns the number written to out. */
+static int32_t bselect(const or_bgraph *g, const or_went *cand, int32_t nc, int32_t m, int32_t keep_pruned,
+                       int32_t *out, int32_t *pruned) {
+  int32_t ns = 0, np = 0;
+  for (int32_t i = 0; i < nc && ns < m; ++i) {
+    int32_t good = 1;
+    for (int32_t j = 0; j < ns; ++j)
+      if (bdist(g, cand[i].id, out[j]) < cand[i].d) { good = 0; break; }
+    if (good) out[ns++] = cand[i].id;
+    else if (keep_pruned) pruned[np++] = cand[i].id;
+  }
+  for (int32_t i = 0; i < np && ns < m; ++i) out[ns++] = pruned[i];
+  return ns;
+}
+
+typedef struct { int32_t L, target, src; } or_rev;
+static int cmp_rev(const void *a, const void *b) {
+  const or_rev *x = (const or_rev *)a, *y = (const or_rev *)b;
+  if (x->L != y->L) return x->L < y->L ? -1 : 1;
+  if (x->target != y->target) return x->target < y->target ? -1 : 1;
+  return (x->src > y->src) - (x->src < y->src);
+}
+static int cmp_went(const void *a, const void *b) {
+  const or_went *x = (const or_went *)a, *y = (const or_went *)b;
+  if (x->d != y->d) return x->d < y->d ? -1 : 1;
+  return (x->id > y->id) - (x->id < y->id);
+}
+
+/* Build the graph.  upper_off (out): row of (v, layer 1) in adj_upper, rows of a node consecutive,
+ * nodes in id order; adj0 [n x 2M], adj_upper [sum of levels x M] -1 padded (caller-sized, see
+ * or_build_upper_rows).  flags bit 0: keep pruned connections; bit 1: a new node selects 2M (not M)
+ * layer-0 neighbours.  batch_div: batch = min(max(1, pos / batch_div), 4096) nodes (R28); a node
+ * that raises the top level is inserted alone.  entry_max (out) = {entry point, max level}. */
+int64_t or_build_upper_rows(const int32_t *levels, int64_t n, int64_t *upper_off) {
+  int64_t rows = 0;
+  for (int64_t i = 0; i < n; ++i) { upper_off[i] = levels[i] > 0 ? rows : -1; rows += levels[i]; }
+  return rows;
+}
+
+int or_build_graph(const uint8_t *codes, int64_t n, int32_t d, int32_t d_pad, const int32_t *levels,
+                   const int64_t *upper_off, int32_t M, int32_t efc, int32_t flags, int32_t batch_div,
+                   int32_t *adj0, int32_t *adj_upper, int32_t *entry_max) {
+  if (!codes || n < 1 || M < 2 || efc < 1 || !adj0 || !entry_max) return OR_EINVAL;
+  const int32_t keep_pruned = flags & 1, sel0 = (flags & 2) ? 2 * M : M, cap0 = 2 * M;
+  if (batch_div <= 0) batch_div = 32;
+  int64_t rows = 0;
+  for (int64_t i = 0; i < n; ++i) rows += levels[i];
+  for (int64_t i = 0; i < n * cap0; ++i) adj0[i] = -1;
+  for (int64_t i = 0; i < rows * M; ++i) adj_upper[i] = -1;
+  or_bgraph g = {codes, n, d, d_pad, M, cap0, levels, upper_off, adj0, adj_upper, NULL, 0};
+  const int32_t wcap = (efc > cap0 ? efc : cap0) + 4096 + 8;
+  g.stamp = (uint32_t *)calloc((size_t)n, sizeof(uint32_t));
+  or_went *W = (or_went *)malloc(sizeof(or_went) * (size_t)wcap);
+  or_went *E = (or_went *)malloc(sizeof(or_went) * (size_t)wcap);
+  int32_t *sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)wcap);
+  int32_t *pr = (int32_t *)malloc(sizeof(int32_t) * (size_t)wcap);
+  or_rev *rev = (or_rev *)malloc(sizeof(or_rev) * (size_t)4096 * (size_t)(31 * M + sel0));
+  if (!g.stamp || !W || !E || !sel || !pr || !rev) {
+    free(g.stamp); free(W); free(E); free(sel); free(pr); free(rev);
+    return OR_ENOMEM;
+  }
+  int32_t entry = 0, max_level = levels[0];
+  int64_t pos = 1;
+  while (pos < n) {
+    int64_t B = pos / batch_div;
+    if (B < 1) B = 1;
+    if (B > 4096) B = 4096;
+    if (B > n - pos) B = n - pos;
+    for (int64_t i = 0; i < B; ++i)
+      if (levels[pos + i] > max_level) { B = i == 0 ? 1 : i; break; }
+    int64_t nrev = 0;
+    /* phase 1: each node of the batch, on the graph as it stood when the batch began (no node of
+     * the batch is linked from the graph yet, so the batch cannot see itself) */
+    for (int64_t bi = 0; bi < B; ++bi) {
+      const int64_t q = pos + bi;
+      const int32_t lq = levels[q];
+      int32_t cur = entry, dcur = bdist(&g, q, cur);
+      for (int32_t L = max_level; L > lq; --L) {  /* greedy descent above the node's level (O9) */
+        for (;;) {
+          const int32_t *row = brow(&g, cur, L);
+          int32_t best = cur, db = dcur;
+          for (int32_t t = 0; t < M; ++t) {
+            int32_t u = row[t];
+            if (u < 0) break;
+            int32_t du = bdist(&g, q, u);
+            if (key_less(du, u, db, best)) { best = u; db = du; }
+          }
+          if (best == cur) break;
+          cur = best;
+          dcur = db;
+        }
+      }
+      int32_t ne = 1;
+      E[0].d = dcur; E[0].id = cur; E[0].expanded = 0;
+      for (int32_t L = lq < max_level ? lq : max_level; L >= 0; --L) {
+        int32_t nw = bsearch_layer(&g, q, E, ne, efc, L, W);
+        int32_t m = bselect(&g, W, nw, L == 0 ? sel0 : M, keep_pruned, sel, pr);
+        int32_t *row = brow(&g, q, L);
+        for (int32_t t = 0; t < m; ++t) {
+          row[t] = sel[t];
+          rev[nrev].L = L; rev[nrev].target = sel[t]; rev[nrev].src = (int32_t)q; ++nrev;
+        }
+        memcpy(E, W, sizeof(or_went) * (size_t)nw);  /* the next layer starts from this W */
+        ne = nw;
+      }
+    }
+    /* phase 2: reverse links per (layer, target), sources in id order (R28) */
+    qsort(rev, (size_t)nrev, sizeof(or_rev), cmp_rev);
+    for (int64_t a = 0; a < nrev;) {
+      int64_t b = a;
+      while (b < nrev && rev[b].L == rev[a].L && rev[b].target == rev[a].target) ++b;
+      const int32_t L = rev[a].L, e = rev[a].target, cap = L == 0 ? cap0 : M;
+      int32_t *row = brow(&g, e, L);
+      int32_t deg = 0;
+      while (deg < cap && row[deg] >= 0) ++deg;
+      if (deg + (b - a) <= cap) {
+        for (int64_t i = a; i < b; ++i) row[deg++] = rev[i].src;
+      } else {
+        int32_t nc = 0;
+        for (int32_t t = 0; t < deg; ++t) { W[nc].d = bdist(&g, e, row[t]); W[nc].id = row[t]; ++nc; }
+        for (int64_t i = a; i < b; ++i) { W[nc].d = bdist(&g, e, rev[i].src); W[nc].id = rev[i].src; ++nc; }
+        qsort(W, (size_t)nc, sizeof(or_went), cmp_went);
+        int32_t m = bselect(&g, W, nc, cap, keep_pruned, sel, pr);
+        for (int32_t t = 0; t < cap; ++t) row[t] = t < m ? sel[t] : -1;
+      }
+      a = b;
+    }
+    for (int64_t bi = 0; bi < B; ++bi)
+      if (levels[pos + bi] > max_level) { max_level = levels[pos + bi]; entry = (int32_t)(pos + bi); }
+    pos += B;
+  }
+  entry_max[0] = entry;
+  entry_max[1] = max_level;
+  free(g.stamp); free(W); free(E); free(sel); free(pr); free(rev);
+  return OR_OK;
+}
+
 int or_ncount(void) { return OR_NCOUNT; }
 
 /* ------------------------------------------------------------------------------------ */
