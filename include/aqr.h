@@ -222,6 +222,31 @@ aqr_status aqr_merge_topk(const float *dist, const int32_t *ids, int32_t n_lists
 
 /* Thread-local description of the last failure ("" if none). */
 const char *aqr_last_error(void);
+/* ------------------------------------------------------------------------------------ */
+/* aqr_build_graph -- the index build, Alg1 Stage 3 (G.Insert(q_i, i, M_i, ef^c) */
+/* for i = 1..n) on the GPU: HNSW insertion [23] over the quantized     */
+/* codes with the integer distance d^q and (d, id) ties, Malkov's neighbour heuristic        */
+/* (R14), nodes inserted in id order in waves (R28).  The result is byte-identical */
+/* to the oracle's or_build_graph and the host builder for the same inputs.                  */
+/* ------------------------------------------------------------------------------------ */
+/* codes:      device [n x d_pad] u8 (aqr_encode's layout, d_pad = round_up(d, 16))
+ * levels:     host [n], each in [0, 30] (floor(-ln(u) / ln(M)) from seeded draws)
+ * upper_off:  host [n]: row of (v, layer 1), rows of a node consecutive, -1 iff levels[v] = 0;
+ *             upper_rows = sum of levels
+ * M:          degree cap at layers >= 1 (2..80); layer-0 rows hold 2M (M_i of Alg1 l.17)
+ * efc:        ef^construction (Alg1 l.18), 1..1024
+ * flags:      bit 0 keepPrunedConnections (R14); bit 1 a new node selects 2M layer-0 neighbours
+ * batch_div:  wave size = min(max(1, pos / batch_div), 4096) (0 = 32; R28)
+ * adj0:       host out [n x 2M], -1 padded;  adj_upper: host out [upper_rows x M], -1 padded
+ * entry_max:  host out {entry point, top level}
+ * Device memory is allocated and released inside (about n x (d_pad + 8 M + 12) bytes plus a
+ * few hundred MB of wave scratch).  Synchronous: returns when the host arrays are filled.
+ * Errors: AQR_E_INVALID (arguments), AQR_E_OOM, AQR_E_CUDA. */
+aqr_status aqr_build_graph(const uint8_t *codes, int64_t n, int32_t d, int32_t d_pad, const int32_t *levels,
+                           const int64_t *upper_off, int64_t upper_rows, int32_t M, int32_t efc, int32_t flags,
+                           int32_t batch_div, int32_t *adj0, int32_t *adj_upper, int32_t *entry_max,
+                           aqr_stream_t stream);
+
 /* "aqr-b200 <version> (sm_100a) src:<16 hex digits>": the hash of the CUDA sources this
  * library was compiled from (build.py rebuilds when it differs from the sources in the tree). */
 const char *aqr_version(void);

@@ -63,7 +63,7 @@ class Debug(C.Structure):
 LAYOUTS = {"auto": 0, "gather": 1, "inline": 2}
 EXPORTS = ["aqr_encode", "aqr_upload_index", "aqr_index_free", "aqr_index_device_bytes", "aqr_index_layout",
            "aqr_search_workspace_size",
-           "aqr_search", "aqr_rerank", "aqr_merge_topk", "aqr_last_error", "aqr_version"]
+           "aqr_search", "aqr_rerank", "aqr_merge_topk", "aqr_build_graph", "aqr_last_error", "aqr_version"]
 
 _lib = None
 
@@ -85,7 +85,7 @@ def lib():
         L.aqr_index_device_bytes.restype = C.c_size_t
         L.aqr_search_workspace_size.restype = C.c_size_t
         L.aqr_index_layout.restype = C.c_int32
-        for f in ["aqr_encode", "aqr_upload_index", "aqr_search", "aqr_rerank", "aqr_merge_topk"]:
+        for f in ["aqr_encode", "aqr_upload_index", "aqr_search", "aqr_rerank", "aqr_merge_topk", "aqr_build_graph"]:
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -379,4 +379,4 @@ def merge_topk(dist, ids, k=None, stream=None):
     return od, oi
 
 
-from .graph import Graph, build_hnsw, adapt_params  # noqa: E402,F401
+from .graph import Graph, build_hnsw, build_hnsw_gpu, adapt_params  # noqa: E402,F401

@@ -429,6 +429,71 @@ aqr_status aqr_rerank(const aqr_index* ix, const float* q, int64_t nq, int64_t l
   return AQR_OK;
 }
 
+aqr_status aqr_build_graph(const uint8_t* codes, int64_t n, int32_t d, int32_t d_pad, const int32_t* levels,
+                           const int64_t* upper_off, int64_t upper_rows, int32_t M, int32_t efc, int32_t flags,
+                           int32_t batch_div, int32_t* adj0, int32_t* adj_upper, int32_t* entry_max,
+                           aqr_stream_t stream) {
+  aqr::g_err.clear();
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  AQR_CHECK_ARG(codes && levels && upper_off && adj0 && entry_max, "build: null pointer");
+  AQR_CHECK_ARG(n >= 1 && n < (int64_t(1) << 31), "build: need 1 <= n < 2^31");
+  AQR_CHECK_ARG(d >= 1 && d_pad == round_up(d, 16) && d_pad <= 2048, "build: need d_pad = round_up(d, 16) <= 2048");
+  AQR_CHECK_ARG(M >= 2 && M <= 80, "build: need 2 <= M <= 80");
+  AQR_CHECK_ARG(efc >= 1 && efc <= 1024, "build: need 1 <= efc <= 1024");
+  AQR_CHECK_ARG(flags >= 0 && flags <= 3, "build: flags must be in [0, 3]");
+  AQR_CHECK_ARG(batch_div >= 0, "build: batch_div must be >= 0");
+  AQR_CHECK_ARG(upper_rows == 0 || adj_upper, "build: adj_upper missing");
+  int64_t rows = 0;
+  for (int64_t v = 0; v < n; ++v) {
+    AQR_CHECK_ARG(levels[v] >= 0 && levels[v] <= 30, "build: levels must be in [0, 30]");
+    AQR_CHECK_ARG(levels[v] == 0 ? upper_off[v] == -1 : upper_off[v] == rows,
+                  "build: upper_off must list each node's rows consecutively, in node order (-1 for level 0)");
+    rows += levels[v];
+  }
+  AQR_CHECK_ARG(rows == upper_rows && rows < (int64_t(1) << 31), "build: upper_rows must equal the sum of levels");
+  const int32_t d32 = round_up(d, 32), cap0 = 2 * M;
+  uint8_t* c32 = nullptr;
+  int32_t *xn = nullptr, *lv = nullptr, *uo = nullptr, *a0 = nullptr, *au = nullptr;
+  struct Free {  // device buffers are released on every exit path
+    std::vector<void*> p;
+    ~Free() {
+      for (void* q : p) cudaFree(q);
+    }
+  } guard;
+  auto alloc = [&](void** q, size_t bytes) -> cudaError_t {
+    cudaError_t r = cudaMalloc(q, bytes < 16 ? 16 : bytes);
+    if (r == cudaSuccess) guard.p.push_back(*q);
+    return r;
+  };
+  AQR_CUDA(alloc((void**)&c32, (size_t)n * d32), "build: alloc");
+  AQR_CUDA(alloc((void**)&xn, sizeof(int32_t) * (size_t)n), "build: alloc");
+  AQR_CUDA(alloc((void**)&lv, sizeof(int32_t) * (size_t)n), "build: alloc");
+  AQR_CUDA(alloc((void**)&uo, sizeof(int32_t) * (size_t)n), "build: alloc");
+  AQR_CUDA(alloc((void**)&a0, sizeof(int32_t) * (size_t)n * cap0), "build: alloc");
+  AQR_CUDA(alloc((void**)&au, sizeof(int32_t) * (size_t)(rows > 0 ? rows : 1) * M), "build: alloc");
+  std::vector<int32_t> uo_h((size_t)n);
+  for (int64_t v = 0; v < n; ++v) uo_h[(size_t)v] = (int32_t)upper_off[v];
+  if (d32 != d_pad) AQR_CUDA(cudaMemsetAsync(c32, 0, (size_t)n * d32, s), "build: memset");
+  AQR_CUDA(cudaMemcpy2DAsync(c32, d32, codes, d_pad, d_pad, n, cudaMemcpyDeviceToDevice, s), "build: codes");
+  AQR_CUDA(cudaMemcpyAsync(lv, levels, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice, s), "build: levels");
+  AQR_CUDA(cudaMemcpyAsync(uo, uo_h.data(), sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice, s), "build: rows");
+  AQR_CUDA(cudaMemsetAsync(a0, 0xff, sizeof(int32_t) * (size_t)n * cap0, s), "build: memset");
+  AQR_CUDA(cudaMemsetAsync(au, 0xff, sizeof(int32_t) * (size_t)(rows > 0 ? rows : 1) * M, s), "build: memset");
+  aqr::IndexView V{};
+  V.n = n;
+  V.codes = c32;
+  V.d_pad = d32;
+  AQR_CUDA(aqr::launch_code_norms(V, xn, s), "build: code norms");
+  AQR_CUDA(aqr::build_graph_gpu(c32, xn, n, d32, lv, levels, uo, M, efc, flags, batch_div, a0, au, entry_max, s),
+           "build: waves");
+  AQR_CUDA(cudaMemcpyAsync(adj0, a0, sizeof(int32_t) * (size_t)n * cap0, cudaMemcpyDeviceToHost, s), "build: copy");
+  if (rows > 0)
+    AQR_CUDA(cudaMemcpyAsync(adj_upper, au, sizeof(int32_t) * (size_t)rows * M, cudaMemcpyDeviceToHost, s),
+             "build: copy");
+  AQR_CUDA(cudaStreamSynchronize(s), "build: sync");
+  return AQR_OK;
+}
+
 aqr_status aqr_merge_topk(const float* dist, const int32_t* ids, int32_t n_lists, int64_t nq, int32_t k,
                           float* out_dist, int32_t* out_ids, aqr_stream_t stream) {
   aqr::g_err.clear();

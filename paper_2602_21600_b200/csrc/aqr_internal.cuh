@@ -70,5 +70,13 @@ cudaError_t launch_merge(const float* dist, const int32_t* ids, int32_t n_lists,
 size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int warps_per_block);
 cudaError_t launch_build_inline(const IndexView& ix, uint8_t* blk, cudaStream_t s);
 cudaError_t launch_code_norms(const IndexView& ix, int32_t* out, cudaStream_t s);
+// GPU index build (build.cu): codes [n x d_pad32] (d_pad32 a multiple of 32, zero padded), their
+// |x^|^2, levels on device and host, upper_off on device (int32); fills adj0_d [n x 2M] and adj_up_d
+// (both pre-set to -1) and entry_max (host) = {entry point, top level}
+cudaError_t build_graph_gpu(const uint8_t* codes, const int32_t* xnorm, int64_t n, int32_t d_pad32,
+                            const int32_t* levels_d, const int32_t* levels_h, const int32_t* up_off_d, int32_t M,
+                            int32_t efc, int32_t flags, int32_t batch_div, int32_t* adj0_d, int32_t* adj_up_d,
+                            int32_t* entry_max, cudaStream_t s);
+size_t build_smem_bytes(int32_t efc);
 
 }  // namespace aqr

@@ -68,6 +68,32 @@ def build_hnsw(codes: np.ndarray, M: int, efc: int, level_u: np.ndarray, n_threa
     return Graph(M, efc, levels, upper_off, adj0, adj_upper, int(out2[0]), int(out2[1]))
 
 
+def build_hnsw_gpu(codes, d: int, M: int, efc: int, level_u: np.ndarray, flags: int = 0, batch_div: int = 0,
+                   stream=None) -> Graph:
+    """aqr_build_graph: the same graph as build_hnsw (byte for byte), built on the GPU (NEXT-1).
+    codes: the [n, d_pad] u8 CUDA tensor of aqr_encode; level_u: the seeded uniform draws."""
+    from . import lib as _aqr_lib, _dev, _stream, _check
+    import torch
+    pc = _dev(codes, torch.uint8, "codes")
+    n, d_pad = codes.shape
+    level_u = np.ascontiguousarray(level_u, dtype=np.float64)
+    levels = np.zeros(n, np.int32)
+    upper_off = np.zeros(n, np.int64)
+    rows = _hlib().aqr_hnsw_levels(level_u.ctypes.data_as(C.c_void_p), C.c_int64(n), C.c_int32(M),
+                                   levels.ctypes.data_as(C.c_void_p), upper_off.ctypes.data_as(C.c_void_p))
+    adj0 = np.empty((n, 2 * M), np.int32)
+    adj_upper = np.empty((max(rows, 0), M), np.int32)
+    em = np.zeros(2, np.int32)
+    st = _aqr_lib().aqr_build_graph(pc, C.c_int64(n), C.c_int32(d), C.c_int32(d_pad),
+                                    levels.ctypes.data_as(C.c_void_p), upper_off.ctypes.data_as(C.c_void_p),
+                                    C.c_int64(rows), C.c_int32(M), C.c_int32(efc), C.c_int32(flags),
+                                    C.c_int32(batch_div), adj0.ctypes.data_as(C.c_void_p),
+                                    adj_upper.ctypes.data_as(C.c_void_p) if rows > 0 else None,
+                                    em.ctypes.data_as(C.c_void_p), _stream(stream))
+    _check(st, "aqr_build_graph")
+    return Graph(M, efc, levels, upper_off, adj0, adj_upper, int(em[0]), int(em[1]))
+
+
 def density_weights(x_sample: np.ndarray, rho: np.ndarray, literal: bool = False) -> np.ndarray:
     """w_j (Alg1 l.12) -- as printed, w_j = (1/n) sum rho_i is j-independent; R16 takes
     SPEC's density-weighted per-dimension variance, floored at 1e-12, normalised to mean 1.
