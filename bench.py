@@ -40,6 +40,7 @@ TARGET_RECALL = 0.98
 EF_AT_TARGET = {"C1": 64, "C2": 784, "C3": 1536, "C4": 128, "C5": 128}
 LAYOUT = "auto"
 WJ_LITERAL = False  # --wj literal: Alg1 l.12 as printed (NEXT-4 variant; R16)
+BUILDER = "gpu"  # --builder: the index build on the GPU (aqr_build_graph) or the host builder
 BUILD_FLAGS = 1  # host builder: Malkov's keepPrunedConnections (R14)
 
 
@@ -286,19 +287,24 @@ def build_index(w, cfg, rank, world, threads, delta_override=None):
     eta = G.eta_of(wj)
     M, efc = G.adapt_params(w.M0, w.efc0, quant.delta, eta)
     t1 = time.time()
-    if rank == 0:
-        g = G.build_hnsw(codes.cpu().numpy(), M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg=cfg), threads,
-                         flags=BUILD_FLAGS)
-        arrs = [g.levels, g.upper_off, g.adj0, g.adj_upper, np.array([g.entry_point, g.max_level], np.int64)]
+    level_u = synth.level_draws(len(w.x), seed=w.seed, cfg=cfg)
+    if BUILDER == "gpu":
+        # the GPU index build (aqr_build_graph, NEXT-1): deterministic, so every rank builds the
+        # same graph on its own GPU (byte-identical with the host builder and the oracle)
+        g = G.build_hnsw_gpu(codes, w.x.shape[1], M, efc, level_u, flags=BUILD_FLAGS)
     else:
-        arrs = [None] * 5
-    if world > 1:
-        dts = [torch.int32, torch.int64, torch.int32, torch.int32, torch.int64]
-        arrs = [bcast_np(a, world, rank, dt) for a, dt in zip(arrs, dts)]
-        g = G.Graph(M, efc, arrs[0], arrs[1], arrs[2], arrs[3], int(arrs[4][0]), int(arrs[4][1]))
+        if rank == 0:
+            g = G.build_hnsw(codes.cpu().numpy(), M, efc, level_u, threads, flags=BUILD_FLAGS)
+            arrs = [g.levels, g.upper_off, g.adj0, g.adj_upper, np.array([g.entry_point, g.max_level], np.int64)]
+        else:
+            arrs = [None] * 5
+        if world > 1:
+            dts = [torch.int32, torch.int64, torch.int32, torch.int32, torch.int64]
+            arrs = [bcast_np(a, world, rank, dt) for a, dt in zip(arrs, dts)]
+            g = G.Graph(M, efc, arrs[0], arrs[1], arrs[2], arrs[3], int(arrs[4][0]), int(arrs[4][1]))
     t_build = time.time() - t1
     ix = aqr.upload_index(codes, x, quant, g, metric=w.metric, layout=LAYOUT)
-    info = dict(layout=ix.layout, build_flags=BUILD_FLAGS, wj="literal" if WJ_LITERAL else "spec", delta=quant.delta, eta=eta, M=M, efc=efc, p_max=P_MAX[cfg], p_low=quant.p_low, p_high=quant.p_high,
+    info = dict(layout=ix.layout, builder=BUILDER, build_flags=BUILD_FLAGS, wj="literal" if WJ_LITERAL else "spec", delta=quant.delta, eta=eta, M=M, efc=efc, p_max=P_MAX[cfg], p_low=quant.p_low, p_high=quant.p_high,
                 encode_s=round(t_enc, 2), build_s=round(t_build, 2), max_level=g.max_level,
                 index_bytes=ix.device_bytes())
     return x, codes, quant, g, ix, info
@@ -730,8 +736,11 @@ def run_sharded(args):
         torch.cuda.synchronize()
         eta = G.eta_of(G.density_weights(xs[samp], quant.rho.cpu().numpy(), literal=WJ_LITERAL))
         M, efc = G.adapt_params(32, 200, quant.delta, eta)
-        g = G.build_hnsw(codes.cpu().numpy(), M, efc, synth.level_draws(n_shard, cfg="C5", shard=s_), threads,
-                         flags=BUILD_FLAGS)
+        lu = synth.level_draws(n_shard, cfg="C5", shard=s_)
+        if BUILDER == "gpu":
+            g = G.build_hnsw_gpu(codes, 96, M, efc, lu, flags=BUILD_FLAGS)
+        else:
+            g = G.build_hnsw(codes.cpu().numpy(), M, efc, lu, threads, flags=BUILD_FLAGS)
         ix = aqr.upload_index(codes, x, quant, g, metric="l2", id_base=s_ * n_shard, layout=LAYOUT)
         shards.append((x, ix, aqr.Searcher(ix, nq, aqr.make_params(k, **m, visited_bits=args.vbits[0]))))
         # exact ground truth of this shard (global ids), merged across shards below
@@ -959,12 +968,16 @@ def main():
     ap.add_argument("--tau-spread", type=float, default=float("inf"),
                     help="adaptive re-rank depth (P:154, R27): re-rank only the entries of A within (1 + tau) of "
                          "d^a_k (at least k, at most N_rerank); inf = the static N_rerank (default)")
+    ap.add_argument("--builder", default="gpu", choices=["gpu", "host"],
+                    help="graph construction (not timed): gpu = aqr_build_graph (NEXT-1), host = csrc/hnsw_build.cpp; "
+                         "both give the same graph byte for byte")
     ap.add_argument("--wj", default="spec", choices=["spec", "literal"],
                     help="density weights w_j for eta (builder only): spec = SPEC's per-dimension weighted "
                          "variance (R16, default); literal = Alg1 l.12 as printed (eta = 0)")
     args = ap.parse_args()
-    global LAYOUT, WJ_LITERAL
+    global LAYOUT, WJ_LITERAL, BUILDER
     WJ_LITERAL = args.wj == "literal"
+    BUILDER = args.builder
     LAYOUT = args.layout
     if args.warmup < 3:
         log("[bench] warm-up raised to 3 (timing rule)")
