@@ -79,6 +79,12 @@ namespace {
 #ifndef AQR_PREFETCH_ROW
 #define AQR_PREFETCH_ROW 1
 #endif
+#ifndef AQR_FINISH_NOINLINE
+#define AQR_FINISH_NOINLINE 0  // 1: Stages 2-3 out of line (their registers stay out of the beam's allocation)
+#endif
+#ifndef AQR_ADAPTIVE
+#define AQR_ADAPTIVE 1  // 0: compile out the adaptive re-rank depth (A/B of its cost)
+#endif
 #ifndef AQR_MOVE32
 #define AQR_MOVE32 1  // 1: W segments move 32 entries per step (0: 128, four loads in flight per lane)
 #endif
@@ -872,13 +878,36 @@ __device__ __forceinline__ void rows4(const IndexView& ix, const float* qf, cons
   }
 }
 
+// adaptive re-rank depth (R27): the entries of A (sorted keys) with d^a <= (1 + tau_spread)
+// d^a_k, at least k, at most `depth` -- a prefix of A, counted by ballots.  Out of line: inlined,
+// it perturbed the register allocation of the whole search kernel (4.5% slower at C2 even when
+// unused, measured)
+__device__ __noinline__ int adaptive_depth(const uint64_t* akeys, int nc, int k, double tau_spread, int depth,
+                                           int lane) {
+  const int kk = k < nc ? k : nc;
+  const double thr = __dmul_rn((double)fkey_inv((uint32_t)(akeys[kk - 1] >> 32)), __dadd_rn(1.0, tau_spread));
+  int band = 0;
+  for (int i0 = 0; i0 < nc; i0 += 32) {
+    const int i = i0 + lane;
+    const bool in = i < nc && (double)fkey_inv((uint32_t)(akeys[i] >> 32)) <= thr;
+    band += __popc(__ballot_sync(kFull, in));
+  }
+  if (band < kk) band = kk;
+  return band < depth ? band : depth;
+}
+
 // ------------------------------------------------------------------------------------
 // Stages 2 / ET / 3 / assembly for one query (Alg2 l.8-24).  cid[0:nc] in smem holds C in
 // (d^q, id) order; region holds >= 20*nc bytes of scratch after cid.
 // ------------------------------------------------------------------------------------
 // C comes either as ids (cid) or as the first nc W keys (wk, which may alias rkeys: entry i is
 // read before it is overwritten).  akeys / rkeys: nc 64-bit keys each.
-__device__ void finish_query(const IndexView& ix, const SearchCfg& c, const float* qf, const int32_t* cid,
+#if AQR_FINISH_NOINLINE
+__device__ __noinline__
+#else
+__device__
+#endif
+void finish_query(const IndexView& ix, const SearchCfg& c, const float* qf, const int32_t* cid,
                              const uint64_t* wk, int nc, uint64_t* akeys, uint64_t* rkeys, int64_t qi,
                              int32_t* out_ids, float* out_dist, const aqr_debug& dbg, bool has_dbg, int lane,
                              int32_t* cnt) {
@@ -910,20 +939,7 @@ __device__ void finish_query(const IndexView& ix, const SearchCfg& c, const floa
     term = (gap > c.tau_gap) || (ratio > c.tau_ratio);
   }
   int depth = c.n_rerank < nc ? c.n_rerank : nc;
-  if (!isinf(c.tau_spread) && nc > 0) {
-    // adaptive depth (R27): the entries of A (sorted) with d^a <= (1 + tau_spread) d^a_k,
-    // at least k, at most N_rerank -- a prefix of A, counted by ballots
-    const int kk = k < nc ? k : nc;
-    const double thr = __dmul_rn((double)fkey_inv((uint32_t)(akeys[kk - 1] >> 32)), __dadd_rn(1.0, c.tau_spread));
-    int band = 0;
-    for (int i0 = 0; i0 < nc; i0 += 32) {
-      const int i = i0 + lane;
-      const bool in = i < nc && (double)fkey_inv((uint32_t)(akeys[i] >> 32)) <= thr;
-      band += __popc(__ballot_sync(kFull, in));
-    }
-    if (band < kk) band = kk;
-    if (band < depth) depth = band;
-  }
+  if (AQR_ADAPTIVE && !isinf(c.tau_spread) && nc > 0) depth = adaptive_depth(akeys, nc, k, c.tau_spread, depth, lane);
   if (term && depth > k) depth = k;
   // Stage 3: exact distances for A[0:depth] (Alg2 l.19-22)
   for (int i0 = 0; i0 < depth; i0 += 4) {
