@@ -82,6 +82,9 @@ namespace {
 #ifndef AQR_FINISH_NOINLINE
 #define AQR_FINISH_NOINLINE 0  // 1: Stages 2-3 out of line (their registers stay out of the beam's allocation)
 #endif
+#ifndef AQR_KNOWN_NEXT
+#define AQR_KNOWN_NEXT 1  // 1: the next expansion's W position carried over (no pick scan)
+#endif
 #ifndef AQR_ADAPTIVE
 #define AQR_ADAPTIVE 1  // 0: compile out the adaptive re-rank depth (A/B of its cost)
 #endif
@@ -1218,9 +1221,16 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       __syncwarp();
     }
     int size = 1, cursor = 0, nexp = 0;
+    // AQR_KNOWN_NEXT: the position of the next expansion, known from the previous one (-1: scan
+    // from the cursor, -2: W has no unexpanded entry left)
+    int npos = -1;
     for (;;) {
       // smallest unexpanded entry of W
       int pos = -1, gpos = -1;
+      if (AQR_KNOWN_NEXT && !AQR_SPEC2 && AQR_W_SLACK == 0 && npos != -1) {
+        if (npos < 0) break;
+        pos = npos;
+      } else
       for (int bb = cursor; bb < size; bb += 32) {
         const int i = bb + lane;
         const bool un = i < size && !(W[i] & 1ull);
@@ -1391,16 +1401,22 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         // never speculative: this node IS expanded next)
         cmin = warp_min_u64(cmin);
         uint64_t kw = ~0ull;
+        int kwpos = -1;
         for (int bb = pos + 1; bb < size; bb += 32) {
           const int i = bb + lane;
           const bool un = i < size && !(W[i] & 1ull);
           const uint32_t mk = __ballot_sync(kFull, un);
           if (mk) {
-            kw = W[bb + __ffs(mk) - 1];
+            kwpos = bb + __ffs(mk) - 1;
+            kw = W[kwpos];
             break;
           }
         }
         const uint64_t nxt = kw < cmin ? kw : cmin;
+        // where the next expansion will sit after this one's merge: an old entry keeps its
+        // position (every new key is larger than it), the smallest new key lands at its
+        // insertion point slb[0]
+        npos = nxt == ~0ull ? -2 : (kw < cmin ? kwpos : -3);
         __syncwarp();
         if (INL) {
           if (nxt != ~0ull && lane == 0) {
@@ -1451,6 +1467,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
       }
       __syncwarp();
       const int first_ins = slb[0];
+      if (npos == -3) npos = first_ins;
       // move whichever side of the insertion points is shorter: the entries after the first
       // one right (tail), or those before the last one left into the free head slots (head)
       bool head = AQR_W_SLACK > 0 && slb[np - 1] < size - first_ins && np <= AQR_W_SLACK;
