@@ -82,6 +82,9 @@ namespace {
 #ifndef AQR_FINISH_NOINLINE
 #define AQR_FINISH_NOINLINE 0  // 1: Stages 2-3 out of line (their registers stay out of the beam's allocation)
 #endif
+#ifndef AQR_HASH_DIRECT
+#define AQR_HASH_DIRECT 1  // 1: the shared-memory visited set is direct-mapped (0: 8-probe open addressing)
+#endif
 #ifndef AQR_KNOWN_NEXT
 #define AQR_KNOWN_NEXT 1  // 1: the next expansion's W position carried over (no pick scan)
 #endif
@@ -748,6 +751,14 @@ __device__ __forceinline__ void fp_dists(const IndexView& ix, const float* qf, c
 // an id that was inserted, and a hit requires the exact id.
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ bool visit_new(uint32_t* h, int hbits, int32_t u, int& fails) {
+#if AQR_HASH_DIRECT
+  // direct-mapped: one slot per id hash, no probing, no atomics (the warp owns its table; two
+  // lanes racing for a slot both report "new" and one id stays -- never a false positive)
+  const uint32_t s0 = ((uint32_t)u * 2654435761u) >> (32 - hbits);
+  if (h[s0] == (uint32_t)u) return false;
+  h[s0] = (uint32_t)u;
+  return true;
+#endif
   const uint32_t hmask = (1u << hbits) - 1u;
   uint32_t s = ((uint32_t)u * 2654435761u) >> (32 - hbits);
 #pragma unroll 1
