@@ -92,7 +92,7 @@ namespace {
 #define AQR_ADAPTIVE 1  // 0: compile out the adaptive re-rank depth (A/B of its cost)
 #endif
 #ifndef AQR_MOVE32
-#define AQR_MOVE32 1  // 1: W segments move 32 entries per step (0: 128, four loads in flight per lane)
+#define AQR_MOVE32 2  // W segments move top first: 2 = 64 entries per step (measured best), 1 = 32, 0 = 128
 #endif
 #ifndef AQR_FUSED_FILTER
 #define AQR_FUSED_FILTER 1  // 1: layer-0 scoring and the max-W filter in one pass (list_filter)
@@ -1555,6 +1555,27 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         // 32 entries per step, top first: one load and one store per lane.  The store of a
         // step lands above its own loads (shift >= 1), never on entries still to be read, so
         // one __syncwarp (loads before stores) per step suffices
+#if AQR_MOVE32 == 2
+        // two 32-entry chunks per step (64 entries: two loads in flight, one __syncwarp)
+        for (; hi - 32 > seg_lo; hi -= 64) {
+          const int p1 = hi - 32 + lane, p0 = hi - 64 + lane;
+          const bool in0 = p0 >= seg_lo;
+          const uint64_t v1 = W[p1];
+          uint64_t v0 = 0;
+          if (in0) v0 = W[p0];
+          __syncwarp();
+          W[p1 + sh] = v1;
+          if (in0) W[p0 + sh] = v0;
+        }
+        if (hi > seg_lo) {
+          const int p = hi - 32 + lane;
+          const bool in = p >= seg_lo;
+          uint64_t v = 0;
+          if (in) v = W[p];
+          __syncwarp();
+          if (in) W[p + sh] = v;
+        }
+#else
         for (; hi > seg_lo; hi -= 32) {
           const int p = hi - 32 + lane;
           const bool in = p >= seg_lo;
@@ -1563,6 +1584,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
           __syncwarp();
           if (in) W[p + sh] = v;
         }
+#endif
         __syncwarp();
         seg_hi = seg_lo;
         continue;
