@@ -304,10 +304,27 @@ def build_index(w, cfg, rank, world, threads, delta_override=None):
             g = G.Graph(M, efc, arrs[0], arrs[1], arrs[2], arrs[3], int(arrs[4][0]), int(arrs[4][1]))
     t_build = time.time() - t1
     ix = aqr.upload_index(codes, x, quant, g, metric=w.metric, layout=LAYOUT)
-    info = dict(layout=ix.layout, builder=BUILDER, build_flags=BUILD_FLAGS, wj="literal" if WJ_LITERAL else "spec", delta=quant.delta, eta=eta, M=M, efc=efc, p_max=P_MAX[cfg], p_low=quant.p_low, p_high=quant.p_high,
+    reach = layer0_reach(g) if rank == 0 else None
+    info = dict(layout=ix.layout, reach_layer0=reach, builder=BUILDER, build_flags=BUILD_FLAGS, wj="literal" if WJ_LITERAL else "spec", delta=quant.delta, eta=eta, M=M, efc=efc, p_max=P_MAX[cfg], p_low=quant.p_low, p_high=quant.p_high,
                 encode_s=round(t_enc, 2), build_s=round(t_build, 2), max_level=g.max_level,
                 index_bytes=ix.device_bytes())
     return x, codes, quant, g, ix, info
+
+
+def layer0_reach(g):
+    """Share of the nodes reachable from the entry point on layer 0 (BFS; SPEC S:431's >= 99%): a
+    recall ceiling of the graph itself, whatever the search does."""
+    n = g.adj0.shape[0]
+    seen = np.zeros(n, bool)
+    seen[g.entry_point] = True
+    front = np.array([g.entry_point])
+    while len(front):
+        nb = g.adj0[front].ravel()
+        nb = np.unique(nb[nb >= 0])
+        nb = nb[~seen[nb]]
+        seen[nb] = True
+        front = nb
+    return round(float(seen.mean()), 6)
 
 
 def bytes_per_query(tot, nq, d, k, distinct_ratio=1.0, traversal="aqr"):
