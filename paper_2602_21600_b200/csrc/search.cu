@@ -85,6 +85,9 @@ namespace {
 #ifndef AQR_HASH_DIRECT
 #define AQR_HASH_DIRECT 1  // 1: the shared-memory visited set is direct-mapped (0: 8-probe open addressing)
 #endif
+#ifndef AQR_VBM_HINT
+#define AQR_VBM_HINT 1  // 1: visited-bitmap atomics carry an L2 evict-last policy
+#endif
 #ifndef AQR_KNOWN_NEXT
 #define AQR_KNOWN_NEXT 1  // 1: the next expansion's W position carried over (no pick scan)
 #endif
@@ -794,6 +797,27 @@ __device__ __forceinline__ int gather_row(const int32_t* row, int cap, int32_t* 
   return m;
 }
 
+// visited-bitmap test-and-set (atomicOr) with an L2 evict-last policy (AQR_VBM_HINT): every
+// warp's bitmap is touched all over during a query (C4: ~20k of its 31k words), the bitmaps of
+// the running queries together are about L2-sized, and the code rows streaming through L2 would
+// otherwise evict them -- each test then became a DRAM round trip (C4: L2 hit rate 20%)
+__device__ __forceinline__ uint64_t vbm_policy() {
+  uint64_t pol = 0;
+#if AQR_VBM_HINT
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+__device__ __forceinline__ uint32_t vbm_test_set(uint32_t* w, uint32_t bit, uint64_t pol) {
+#if AQR_VBM_HINT
+  uint32_t old;
+  asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(w), "r"(bit), "l"(pol) : "memory");
+  return old;
+#else
+  return atomicOr(w, bit);
+#endif
+}
+
 // rank sort of n 64-bit distinct keys: dst[rank(src[i])] = src[i]
 __device__ __forceinline__ void rank_sort(const uint64_t* src, uint64_t* dst, int n, int lane) {
   for (int i = lane; i < n; i += 32) {
@@ -1096,6 +1120,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
   // visited_bits = -2: this warp slot's bitmap in global memory (exact; no shared memory)
   uint32_t* vbm = (!INL && c.vbm) ? c.vbm + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * c.vbm_words
                                   : nullptr;
+  const uint64_t vpol = vbm ? vbm_policy() : 0ull;
   const int sub = lane % LPR;
   const int nch = ix.d_pad >> 5;
   const int ef = c.ef;
@@ -1325,7 +1350,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
 #pragma unroll
           for (int t = 0; t < kRowRegs; ++t) {
             const int32_t u = arow[t];
-            old[t] = (32 * t < ix.cap0 && u >= 0) ? atomicOr(vbm + (u >> 5), 1u << (u & 31)) : ~0u;
+            old[t] = (32 * t < ix.cap0 && u >= 0) ? vbm_test_set(vbm + (u >> 5), 1u << (u & 31), vpol) : ~0u;
           }
 #pragma unroll
           for (int t = 0; t < kRowRegs; ++t) {
