@@ -69,7 +69,9 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB_AQR
+    """libaqr.so, or libaqr_<v>.so when AQR_LIB_VARIANT=v (a test build, e.g. the bounds-checked one)."""
+    v = os.environ.get("AQR_LIB_VARIANT")
+    return os.path.join(_PKG, f"libaqr_{v}.so") if v else _build.LIB_AQR
 
 
 def lib():

@@ -23,6 +23,7 @@
 // 1e-5 relative (north_star tolerance); the fp32 baseline uses the canonical order R(L) and
 // is bit-exact.  Compile-time AQR_* knobs below record measured alternatives.
 #include <cfloat>
+#include <cstdio>
 #include <climits>
 
 #include "aqr_internal.cuh"
@@ -103,6 +104,27 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kEmpty = 0xffffffffu;
+
+// AQR_CHECKS=1 (a test build, libaqr_checked.so): bounds checks on every shared-memory array
+// index and every gathered node id; a violation prints its line and traps.  compute-sanitizer is
+// closed on this pool, so the GPU suite runs against this build instead (tools/gpu/checked.sh)
+#ifndef AQR_CHECKS
+#define AQR_CHECKS 0
+#endif
+#if AQR_CHECKS
+#define AQR_ASSERT(cond)                                                                     \
+  do {                                                                                       \
+    if (!(cond)) {                                                                           \
+      printf("AQR_CHECKS: %s failed at search.cu:%d (block %d thread %d)\n", #cond, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                            \
+      __trap();                                                                              \
+    }                                                                                        \
+  } while (0)
+#else
+#define AQR_ASSERT(cond) \
+  do {                   \
+  } while (0)
+#endif
 constexpr int kProbes = 8;
 
 // ------------------------------------------------------------------------------------
@@ -493,6 +515,7 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg
     for (int u = 0; u < U; ++u) {
       const int r = r0 + g * U + u;
       const int id = r < m ? idv[u] : -1;
+      AQR_ASSERT(id < ix.n);
       const uint8_t* row = ix.codes + (int64_t)(id < 0 ? 0 : id) * ix.d_pad;
 #pragma unroll
       for (int t = 0; t < CPL; ++t) {
@@ -566,6 +589,7 @@ __device__ __forceinline__ int list_filter(const IndexView& ix, const C32 (&qreg
       const int idv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
+        AQR_ASSERT(idv[e] < ix.n && alt < ix.n);
         const uint8_t* row = ix.codes + (uint64_t)(uint32_t)(idv[e] >= 0 ? idv[e] : alt) * dpad;
 #pragma unroll
         for (int t = 0; t < CPL; ++t) ldg256_keep(row + 32 * min(sub + LPR * t, nch - 1), buf[u4 + e][t]);
@@ -589,6 +613,7 @@ __device__ __forceinline__ int list_filter(const IndexView& ix, const C32 (&qreg
       const uint64_t kk = ((uint64_t)(uint32_t)(qq + part[v] + xn[v]) << 32) | ((uint64_t)(uint32_t)id << 1);
       const bool ok = (REP == 1 || (sub % REP) == 0) && id >= 0 && kk < maxk;
       const uint32_t mk = __ballot_sync(kFull, ok);
+      AQR_ASSERT(!ok || np0 + __popc(mk & lt) < m + 32);
       if (ok) cs[np0 + __popc(mk & lt)] = kk;
       np0 += __popc(mk);
     }
@@ -954,6 +979,8 @@ void finish_query(const IndexView& ix, const SearchCfg& c, const float* qf, cons
     int32_t id[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) id[r] = i0 + r < nc ? (cid ? cid[i0 + r] : qkey_id(wk[i0 + r])) : -1;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) AQR_ASSERT(id[r] < ix.n);
     float da[4];
     rows4<false>(ix, qf, id, lane, da);
     __syncwarp();  // wk may alias rkeys: these entries are read before they are overwritten
@@ -1293,8 +1320,10 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
           if (32 * t < ix.cap0 && j < ix.cap0) arow2[t] = __ldg(ix.adj0 + rb2 + j);
         }
       }
+      AQR_ASSERT(pos >= 0 && pos < size && size <= ef);
       const uint64_t wk = W[pos];
       const int32_t cnode = qkey_id(wk);
+      AQR_ASSERT(cnode >= 0 && cnode < ix.n && !(wk & 1ull));
       __syncwarp();
       if (lane == 0) {
         W[pos] = wk | 1ull;
@@ -1336,8 +1365,10 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
           // the row as it is: -1 entries are skipped by the gather and the filter
           m = ix.cap0;
 #pragma unroll
-          for (int t = 0; t < kRowRegs; ++t)
+          for (int t = 0; t < kRowRegs; ++t) {
+            AQR_ASSERT(arow[t] < ix.n && lane + 32 * t < H::NB);
             if (32 * t < ix.cap0) nb[lane + 32 * t] = arow[t];
+          }
           if (has_dbg) {
 #pragma unroll
             for (int t = 0; t < kRowRegs; ++t)
@@ -1350,6 +1381,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
 #pragma unroll
           for (int t = 0; t < kRowRegs; ++t) {
             const int32_t u = arow[t];
+            AQR_ASSERT(u < 0 || (u < ix.n && (int64_t)(u >> 5) < c.vbm_words));
             old[t] = (32 * t < ix.cap0 && u >= 0) ? vbm_test_set(vbm + (u >> 5), 1u << (u & 31), vpol) : ~0u;
           }
 #pragma unroll
@@ -1359,6 +1391,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
             deg += __popc(__ballot_sync(kFull, u >= 0));
             const bool keep = u >= 0 && !(old[t] & (1u << (u & 31)));
             const uint32_t mk = __ballot_sync(kFull, keep);
+            AQR_ASSERT(!keep || m + __popc(mk & ((1u << lane) - 1u)) < H::NB);
             if (keep) nb[m + __popc(mk & ((1u << lane) - 1u))] = u;
             m += __popc(mk);
           }
@@ -1371,6 +1404,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
             bool keep = u >= 0;
             if (keep && vhash) keep = visit_new(hash, c.hbits, u, fails);
             const uint32_t mk = __ballot_sync(kFull, keep);
+            AQR_ASSERT(!keep || m + __popc(mk & ((1u << lane) - 1u)) < H::NB);
             if (keep) nb[m + __popc(mk & ((1u << lane) - 1u))] = u;
             m += __popc(mk);
           }
@@ -1423,6 +1457,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         const uint32_t mk = __ballot_sync(kFull, ok);
         if (ok) {
           const int jj = np + __popc(mk & ((1u << lane) - 1u));
+          AQR_ASSERT(jj < CAP && lb >= 0 && lb <= size);
           cand[jj] = kk;
           clb[jj] = lb;
           cmin = kk < cmin ? kk : cmin;
@@ -1498,6 +1533,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         int r = 0;
 #pragma unroll 4
         for (int j = 0; j < np; ++j) r += cand[j] < kk;
+        AQR_ASSERT(r < np && np <= CAP);
         cs[r] = kk;
         slb[r] = clb[i];
       }
@@ -1589,6 +1625,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
           uint64_t v0 = 0;
           if (in0) v0 = W[p0];
           __syncwarp();
+          AQR_ASSERT(p1 >= seg_lo && p1 + sh < ef);
           W[p1 + sh] = v1;
           if (in0) W[p0 + sh] = v0;
         }
@@ -1633,6 +1670,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         seg_hi = seg_lo;
       }
       for (int j = lane; j < np; j += 32) {
+        AQR_ASSERT(slb[j] >= 0 && slb[j] <= size);
         if (slb[j] + j < ef) W[slb[j] + j] = cs[j];
       }
       __syncwarp();
