@@ -523,31 +523,57 @@ def run_aqr(args):
         ratio = 1.0  # a visited set: the kernel's evaluation count is already the distinct one
     bq = bytes_per_query(tot_counters, len(q), w.x.shape[1], k, ratio, args.kt)
 
-    # ---- device-timed region: W warm-up steps, then K steps bracketed by barrier + sync ----
+    # ---- the search kernel alone: isolated launches on one stream, events around each (the
+    # roofline's kernel time) ----
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+    s.run(q)
+    torch.cuda.synchronize()
+    iso = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(max(3, args.steps))]
+    for a, b in iso:
+        a.record(stream)
         s.run(q)
+        b.record(stream)
+    torch.cuda.synchronize()
+    launch_ms = float(np.mean([a.elapsed_time(b) for a, b in iso]))
+
+    # ---- device-timed region: W warm-up steps, then K steps bracketed by barrier + sync.  Steps
+    # are issued round-robin on P streams (--pipeline, default 2), each with its own Searcher
+    # (outputs + workspace), so the persistent grid's tail of one step overlaps the start of the
+    # next, as consecutive batches of a serving loop do; every step searches its whole batch ----
+    P = max(1, args.pipeline)
+    searchers = [s] + [aqr.Searcher(ix, len(q), p) for _ in range(P - 1)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+
+    def run_steps(nsteps, gate):
+        for st in streams:
+            st.wait_event(gate)
+        for i in range(nsteps):
+            searchers[i % P].run(q, stream=streams[i % P])
+        for st in streams:
+            stream.wait_stream(st)
+
+    g0 = torch.cuda.Event()
+    g0.record(stream)
+    run_steps(args.warmup, g0)
     torch.cuda.synchronize()
     barrier(world)
     clocks = Clocks(local)
     clocks.start()
     barrier(world)
     torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    for a, b in evs:
-        a.record(stream)
-        s.run(q)
-        b.record(stream)
+    run_steps(args.steps, t_start)
     t_end.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     clk = clocks.stop()
     total_ms = t_start.elapsed_time(t_end)
-    launch_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
     total_ms = allreduce_max(total_ms, world)
+    # every step's results are the searchers' (identical queries -> identical results)
+    for sx in searchers[1:]:
+        assert torch.equal(sx.ids, s.ids), "pipelined searchers disagree"
     ms_per_step = total_ms / args.steps
     queries_per_step_all = queries_all  # distinct queries searched by all ranks in one step
     value = queries_per_step_all / (ms_per_step / 1e3)
@@ -557,20 +583,32 @@ def run_aqr(args):
     ids_h = torch.empty((len(q), k), dtype=torch.int32).pin_memory()
     dist_h = torch.empty((len(q), k), dtype=torch.float32).pin_memory()
     qd = torch.empty_like(q)
-    for _ in range(2):
-        qd.copy_(qh, non_blocking=True)
-        s.run(qd)
-        ids_h.copy_(s.ids, non_blocking=True)
-        dist_h.copy_(s.dist, non_blocking=True)
+    # per pipeline stream: its own device query buffer and pinned host outputs
+    qds = [qd] + [torch.empty_like(q) for _ in range(P - 1)]
+    outs_h = [(ids_h, dist_h)] + [(torch.empty_like(ids_h).pin_memory(), torch.empty_like(dist_h).pin_memory())
+                                  for _ in range(P - 1)]
+
+    def e2e_steps(nsteps, gate):
+        for st in streams:
+            st.wait_event(gate)
+        for i in range(nsteps):
+            j = i % P
+            with torch.cuda.stream(streams[j]):
+                qds[j].copy_(qh, non_blocking=True)
+                searchers[j].run(qds[j], stream=streams[j])
+                outs_h[j][0].copy_(searchers[j].ids, non_blocking=True)
+                outs_h[j][1].copy_(searchers[j].dist, non_blocking=True)
+        for st in streams:
+            stream.wait_stream(st)
+
+    g1 = torch.cuda.Event()
+    g1.record(stream)
+    e2e_steps(2 * P, g1)
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        qd.copy_(qh, non_blocking=True)
-        s.run(qd)
-        ids_h.copy_(s.ids, non_blocking=True)
-        dist_h.copy_(s.dist, non_blocking=True)
+    e2e_steps(args.steps, e0)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = allreduce_max(e0.elapsed_time(e1) / args.steps, world)
@@ -644,9 +682,14 @@ def run_aqr(args):
                                          None),
                        "visited_bits": best_vb, "visited_bits_sweep": vb_results, "queries_per_rank": len(q),
                        "parallelism": f"replicated index, query-parallel over {world} GPU(s), no data-path collective",
-                       "l2": "index (codes+adjacency+fp32) > 126 MB L2; no flush", **info},
+                       "l2": "index (codes+adjacency+fp32) > 126 MB L2; no flush",
+                       "pipeline": P, "pipeline_note": ("steps issued round-robin on this many CUDA streams, each "
+                                                        "with its own outputs and workspace: one step's grid tail "
+                                                        "overlaps the next step's start; roofline.kernel_ms is an "
+                                                        "isolated single-stream launch"), **info},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "frac_pipelined": round(bytes_launch / (ms_per_step / 1e3) / 1e9 / peak, 4),
                          "bytes_per_query": round(bq, 1), "peak_source": peak_src,
                          "distinct_eval_ratio": round(ratio, 4), "distinct_ratio_sample": n_ratio,
                          "kernel": "search_kernel", "kernel_ms": round(launch_ms, 4)},
@@ -655,6 +698,7 @@ def run_aqr(args):
                     "h2d_bytes_per_step": h2d_all, "d2h_bytes_per_step": d2h_all,
                     "note": "all ranks; pinned host queries in and ids + distances out inside the timed region"},
             "gpu_launches": args.steps,
+            "ms_per_step_isolated": round(launch_ms, 4),
             "steady_state": steady,
             "clocks": clk,
             "ef_sweep": sweep,
@@ -997,6 +1041,9 @@ def main():
     ap.add_argument("--tau-spread", type=float, default=float("inf"),
                     help="adaptive re-rank depth (P:154, R27): re-rank only the entries of A within (1 + tau) of "
                          "d^a_k (at least k, at most N_rerank); inf = the static N_rerank (default)")
+    ap.add_argument("--pipeline", type=int, default=2,
+                    help="C1-C4: streams the timed steps are issued on, round-robin (1 = back to back on one "
+                         "stream); each stream has its own Searcher, so a step's tail overlaps the next step")
     ap.add_argument("--builder", default="gpu", choices=["gpu", "host"],
                     help="graph construction (not timed): gpu = aqr_build_graph (NEXT-1), host = csrc/hnsw_build.cpp; "
                          "both give the same graph byte for byte")
