@@ -96,7 +96,7 @@ namespace {
 #define AQR_ADAPTIVE 1  // 0: compile out the adaptive re-rank depth (A/B of its cost)
 #endif
 #ifndef AQR_MOVE32
-#define AQR_MOVE32 2  // W segments move top first: 2 = 64 entries per step (measured best), 1 = 32, 0 = 128
+#define AQR_MOVE32 3  // W segments move top first: 3 = 128 per step while long, then 64 (2 = 64 only, 1 = 32, 0 = 128)
 #endif
 #ifndef AQR_FUSED_FILTER
 #define AQR_FUSED_FILTER 1  // 1: layer-0 scoring and the max-W filter in one pass (list_filter)
@@ -1616,7 +1616,20 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_k
         // 32 entries per step, top first: one load and one store per lane.  The store of a
         // step lands above its own loads (shift >= 1), never on entries still to be read, so
         // one __syncwarp (loads before stores) per step suffices
-#if AQR_MOVE32 == 2
+#if AQR_MOVE32 == 3
+        // four unpredicated 32-entry chunks per step while the segment is long (C3 ef 4096: 265.9 ->
+        // 253.5 ms; C2 ef 784: 9.76 -> 9.79, within noise.  Gated by a runtime ef test it cost C2 2.7%)
+        for (; hi - 128 >= seg_lo; hi -= 128) {
+          const uint64_t v3 = W[hi - 32 + lane], v2 = W[hi - 64 + lane], v1 = W[hi - 96 + lane],
+                         v0 = W[hi - 128 + lane];
+          __syncwarp();
+          W[hi - 32 + lane + sh] = v3;
+          W[hi - 64 + lane + sh] = v2;
+          W[hi - 96 + lane + sh] = v1;
+          W[hi - 128 + lane + sh] = v0;
+        }
+#endif
+#if AQR_MOVE32 >= 2
         // two 32-entry chunks per step (64 entries: two loads in flight, one __syncwarp)
         for (; hi - 32 > seg_lo; hi -= 64) {
           const int p1 = hi - 32 + lane, p0 = hi - 64 + lane;
