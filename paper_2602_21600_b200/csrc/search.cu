@@ -89,6 +89,9 @@ namespace {
 #ifndef AQR_VBM_HINT
 #define AQR_VBM_HINT 1  // 1: visited-bitmap atomics carry an L2 evict-last policy
 #endif
+#ifndef AQR_WIDE_U
+#define AQR_WIDE_U 16  // > 0: wide-row kernels (LPR 32) read this many rows per pass, registers unbounded (0: 8, 80 regs)
+#endif
 #ifndef AQR_KNOWN_NEXT
 #define AQR_KNOWN_NEXT 1  // 1: the next expansion's W position carried over (no pick scan)
 #endif
@@ -283,9 +286,12 @@ struct Layout {
 __host__ __device__ constexpr int al16(int x) { return (x + 15) & ~15; }
 
 // rows per lane per list_dists pass: AQR_ROWS_PER_PASS 16-byte chunks in flight per lane
-template <int CPL>
+template <int CPL, int LPR = 0>
 __host__ __device__ constexpr int rows_u() {
-  return AQR_ROWS_PER_PASS / (2 * CPL) < 4 ? 4 : AQR_ROWS_PER_PASS / (2 * CPL) / 4 * 4;
+  // wide rows (LPR 32: one row per warp step): AQR_WIDE_U rows per pass, with the register
+  // budget of a few resident warps (see the launch bounds of search_kernel)
+  return (LPR == 32 && AQR_WIDE_U > 0) ? AQR_WIDE_U / CPL
+         : (AQR_ROWS_PER_PASS / (2 * CPL) < 4 ? 4 : AQR_ROWS_PER_PASS / (2 * CPL) / 4 * 4);
 }
 
 // per-query counters + mbarriers at the end of the hot region: live for the whole kernel, so a
@@ -298,7 +304,7 @@ constexpr int kHotTail = 80;
 // per warp
 template <int LPR, int CPL, int CAP, bool NDA = false>
 struct Hot {
-  static constexpr int PASS = (32 / LPR) * rows_u<CPL>();  // rows read per list_dists pass
+  static constexpr int PASS = (32 / LPR) * rows_u<CPL, LPR>();  // rows read per list_dists pass
   static constexpr int NB1 = (CAP + PASS - 1) / PASS * PASS;
   static constexpr int NB = NB1 > (CAP + 31) / 32 * 32 ? NB1 : (CAP + 31) / 32 * 32;
   static constexpr int o_nb = 0;                                  // int32 [NB] neighbour ids
@@ -482,7 +488,7 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg
   constexpr int G = 32 / LPR;
   // all loads of a pass are issued before any is consumed: U rows per lane, G * U rows per pass,
   // so a typical layer-0 expansion (<= 64 rows of 128 B) costs ONE DRAM round trip
-  constexpr int U = rows_u<CPL>();
+  constexpr int U = rows_u<CPL, LPR>();
   static_assert(U % 4 == 0, "U must be a multiple of 4");
   const int g = lane / LPR, sub = lane % LPR;
   const int nch = ix.d_pad >> 5;
@@ -561,7 +567,7 @@ __device__ __forceinline__ int list_filter(const IndexView& ix, const C32 (&qreg
                                            const int32_t* ids, int m, const uint64_t* W, int size, int ef,
                                            uint64_t* cs, int lane) {
   constexpr int G = 32 / LPR;
-  constexpr int U = rows_u<CPL>();
+  constexpr int U = rows_u<CPL, LPR>();
   constexpr int PER = U >= LPR ? U / LPR : 1;
   constexpr int REP = U >= LPR ? 1 : LPR / U;
   const int g = lane / LPR, sub = lane % LPR;
@@ -1122,7 +1128,7 @@ __device__ __forceinline__ void block_dists(const uint8_t* codes_s, int d_pad, c
 // shared-memory visited hash)
 // ------------------------------------------------------------------------------------
 template <int LPR, int CPL, bool INL, int CAP, bool FP, bool DBG>
-__global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, AQR_MIN_CTAS) search_kernel(IndexView ix, SearchCfg c, Layout L, const float* __restrict__ q,
+__global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE_U > 0) ? 1 : AQR_MIN_CTAS) search_kernel(IndexView ix, SearchCfg c, Layout L, const float* __restrict__ q,
                                                      int64_t nq, int64_t ld_q, int32_t* __restrict__ out_ids,
                                                      float* __restrict__ out_dist, aqr_debug dbg, int dbg_flags,
                                                      int* __restrict__ counter) {
