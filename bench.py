@@ -30,7 +30,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-EF_GRID = [16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 640, 768, 896, 1024, 1280, 1536, 2048, 3072, 4096]
+EF_GRID = [16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 640, 768, 896, 1024, 1280, 1536, 2048, 3072, 4096, 6144, 8192]
 # per-config quantizer window P_max (never given by the paper; R4) and the
 # fixed HNSW construction inputs of BASELINE.json
 P_MAX = {"C1": 0.2, "C2": 0.2, "C3": 0.0, "C4": 0.2, "C5": 5.0}

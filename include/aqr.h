@@ -143,7 +143,7 @@ int32_t aqr_index_layout(const aqr_index *ix);
 
 typedef struct {
   int32_t k;            /* results per query (Alg2 l.1) */
-  int32_t ef;           /* layer-0 beam width ef_search (N_c x m_ef, R13) */
+  int32_t ef;           /* layer-0 beam width ef_search (N_c x m_ef, R13), <= 8192 */
   int32_t n_coarse;     /* N_c: |C| handed to Stage 2; k <= n_coarse <= ef */
   int32_t n_rerank;     /* N_rerank: exact re-rank depth (Alg2 l.20); 0 <= n_rerank <= n_coarse */
   double tau_gap;       /* >= 0 */

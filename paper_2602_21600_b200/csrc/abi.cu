@@ -330,7 +330,7 @@ static aqr_status check_search_params(const aqr_search_params* p, bool need_ef) 
   if (need_ef) {
     AQR_CHECK_ARG(p->n_coarse >= p->k, "search: need n_coarse >= k");
     AQR_CHECK_ARG(p->ef >= p->n_coarse, "search: need ef >= n_coarse");
-    AQR_CHECK_ARG(p->ef <= 4096, "search: ef > 4096 unsupported");
+    AQR_CHECK_ARG(p->ef <= 8192, "search: ef > 8192 unsupported");
     AQR_CHECK_ARG(p->n_rerank >= 0 && p->n_rerank <= p->n_coarse, "search: need 0 <= n_rerank <= n_coarse");
   } else {
     AQR_CHECK_ARG(p->n_rerank >= 0, "rerank: need n_rerank >= 0");

@@ -69,7 +69,7 @@ namespace {
 #define AQR_ROWS_PER_PASS 16  // 16-byte code chunks in flight per lane per gather pass
 #endif
 #ifndef AQR_LB_SHAR
-#define AQR_LB_SHAR 1  // 1: W lower bound in Shar's form, probes unrolled (ef <= 8191)
+#define AQR_LB_SHAR 1  // 1: W lower bound in Shar's form, probes unrolled (ef <= 16383)
 #endif
 #ifndef AQR_LB_FIXED
 #define AQR_LB_FIXED 1  // 1: W lower bound with a warp-uniform trip count (no lane divergence)
@@ -242,7 +242,7 @@ __device__ __forceinline__ int lower_bound_w(const uint64_t* a, int n, uint64_t 
 #define AQR_LB_STEP(L) \
   case L:              \
     if (a[i + (1 << ((L)-1)) - 1] < key) i += 1 << ((L)-1);
-    AQR_LB_STEP(12) AQR_LB_STEP(11) AQR_LB_STEP(10) AQR_LB_STEP(9) AQR_LB_STEP(8) AQR_LB_STEP(7)
+    AQR_LB_STEP(13) AQR_LB_STEP(12) AQR_LB_STEP(11) AQR_LB_STEP(10) AQR_LB_STEP(9) AQR_LB_STEP(8) AQR_LB_STEP(7)
     AQR_LB_STEP(6) AQR_LB_STEP(5) AQR_LB_STEP(4) AQR_LB_STEP(3) AQR_LB_STEP(2) AQR_LB_STEP(1)
 #undef AQR_LB_STEP
     default:

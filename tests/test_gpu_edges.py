@@ -33,12 +33,12 @@ def _gpu_index(c, layout="gather"):
     return aqr.upload_index(codes, x, quant, c.graph, metric=c.w.metric, layout=layout)
 
 
-def _compare(c, ix, q, p):
-    """visit order, C and final ids bit-exact; final distances within 1e-5 relative."""
+def _compare(c, ix, q, p, exp_cap=4096):
+    """visit order, C, final ids and final distances bit-exact (R24)."""
     torch = _torch()
     aqr = _aqr()
-    o_ids, o_d, o_tr = oracle.search(c.ix, q, trace=True, exp_cap=4096, **p)
-    g_ids, g_d, g_tr = aqr.search(ix, torch.from_numpy(q).cuda(), trace=True, exp_cap=4096, **p)
+    o_ids, o_d, o_tr = oracle.search(c.ix, q, trace=True, exp_cap=exp_cap, **p)
+    g_ids, g_d, g_tr = aqr.search(ix, torch.from_numpy(q).cuda(), trace=True, exp_cap=exp_cap, **p)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(g_tr["exp_ids"].cpu().numpy(), o_tr["exp_ids"])
     np.testing.assert_array_equal(g_tr["coarse_ids"].cpu().numpy(), o_tr["coarse_ids"])
@@ -47,7 +47,7 @@ def _compare(c, ix, q, p):
     g_d = g_d.cpu().numpy()
     fin = np.isfinite(o_d)
     np.testing.assert_array_equal(np.isfinite(g_d), fin)
-    np.testing.assert_allclose(g_d[fin], o_d[fin], rtol=1e-5, atol=1e-30)
+    np.testing.assert_array_equal(g_d.view(np.uint32), o_d.view(np.uint32))
     return g_ids.cpu().numpy(), g_d
 
 
@@ -106,12 +106,21 @@ def test_one_dimension():
 
 @pytest.mark.parametrize("layout", ["gather", "inline"])
 def test_largest_ef_and_k(layout):
-    # ef = 4096 (the ABI maximum) over a 3000-node index: W holds the whole reachable set;
-    # k = 100 (C5's k) with N_c = N_rerank = 100
+    # ef = 4096 over a 3000-node index: W holds the whole reachable set; k = 100 (C5's k) with
+    # N_c = N_rerank = 100
     from tests._cases import case
     c = case("c1small")
     ix = _gpu_index(c, layout)
     _compare(c, ix, c.w.q[:8], dict(k=100, ef=4096, n_coarse=100, n_rerank=100))
+
+
+def test_ef_8192():
+    # the ABI maximum ef = 8192 (64 KB of W per query: one warp per CTA) on the 60k C2 slice,
+    # where W really fills: the 13-step lower bound, the long W moves and a 2730-entry C
+    from tests._cases import case
+    c = case("c2slice")
+    ix = _gpu_index(c)
+    _compare(c, ix, c.w.q[:6], dict(k=10, ef=8192, n_coarse=2730, n_rerank=2730), exp_cap=16384)
 
 
 def test_argument_errors():
@@ -124,7 +133,7 @@ def test_argument_errors():
         aqr.search(ix, q, k=5, ef=8, n_coarse=10, n_rerank=5)
     with pytest.raises(aqr.AqrError, match="n_coarse >= k"):
         aqr.search(ix, q, k=12, ef=16, n_coarse=10, n_rerank=5)
-    with pytest.raises(aqr.AqrError, match="ef > 4096"):
-        aqr.search(ix, q, k=5, ef=5000, n_coarse=10, n_rerank=5)
+    with pytest.raises(aqr.AqrError, match="ef > 8192"):
+        aqr.search(ix, q, k=5, ef=9000, n_coarse=10, n_rerank=5)
     with pytest.raises(aqr.AqrError):
         aqr.search(ix, q.cpu(), k=5, ef=16, n_coarse=10, n_rerank=5)  # host tensor: no CPU path
