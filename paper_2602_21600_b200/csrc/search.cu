@@ -66,7 +66,7 @@ namespace {
 #define AQR_SEARCH4 0  // 1: 4-ary W lower bound (three probes per step; measured slower at throughput)
 #endif
 #ifndef AQR_ROWS_PER_PASS
-#define AQR_ROWS_PER_PASS 16  // 16-byte code chunks in flight per lane per gather pass
+#define AQR_ROWS_PER_PASS 8  // 16-byte code chunks in flight per lane per gather pass (8: 4 rows of 32 B; 16 measured slower)
 #endif
 #ifndef AQR_LB_SHAR
 #define AQR_LB_SHAR 1  // 1: W lower bound in Shar's form, probes unrolled (ef <= 16383)
