@@ -692,7 +692,7 @@ def run_aqr(args):
                          "frac_pipelined": round(bytes_launch / (ms_per_step / 1e3) / 1e9 / peak, 4),
                          "limiter": ("below the HBM roofline the kernel is bound by per-warp dependent chains and "
                                      "issue (ncu: DRAM ~11% of peak, L2 hit ~78%, issue ~62% busy; "
-                                     "profiles/r02/ncu_search_c2_final*.txt)"),
+                                     "profiles/r02/ncu_search_c2_head*.txt)"),
                          "bytes_per_query": round(bq, 1), "peak_source": peak_src,
                          "distinct_eval_ratio": round(ratio, 4), "distinct_ratio_sample": n_ratio,
                          "kernel": "search_kernel", "kernel_ms": round(launch_ms, 4)},
