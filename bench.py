@@ -1064,8 +1064,9 @@ def main():
     args.kt = "fp32" if args.traversal == "fp32" else "aqr"  # the kernel's traversal
     if args.vbits is None:
         # the exact global visited bitmap (-2) pays where re-evaluations dominate (distinct ratio
-        # 0.03 on C1, 0.09 on C4: measured 2.2x / 3.3x); elsewhere none (R15)
-        args.vbits = {"C1": [-2, -1, 13], "C4": [-2, -1]}.get(args.config, [-1])
+        # 0.03 on C1, 0.09 on C4: measured 2.2x / 3.3x); C5 (0.09 per shard) a 2^10-slot 16-bit-tag
+        # table in shared memory (no occupancy cost: 3.79 -> 2.97 ms per shard); elsewhere none (R15)
+        args.vbits = {"C1": [-2, -1, 13], "C4": [-2, -1], "C5": [10]}.get(args.config, [-1])
     if args.traversal == "sq8":
         args.rerank = "full"
     if args.rerank == "auto":

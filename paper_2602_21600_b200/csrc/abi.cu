@@ -360,6 +360,8 @@ static aqr::SearchCfg make_cfg(const aqr_search_params* p) {
   c.early_term = p->early_term;
   c.assemble_mode = p->assemble_mode;
   c.hbits = p->visited_bits > 0 ? p->visited_bits : 0;
+  c.htag = -1;  // chosen per index by the launcher (hash_params)
+  c.hmul = c.hmaskb = 0u;
   c.vbm = nullptr;  // visited_bits = -2: set by aqr_search from the workspace
   c.vbm_words = 0;
   c.vbm_slots = 0;

@@ -39,6 +39,8 @@ struct SearchCfg {
   double tau_spread;      // adaptive re-rank depth (R27); +inf = static n_rerank
   int32_t early_term, assemble_mode;
   int32_t hbits;          // visited hash slots = 1 << hbits
+  int32_t htag;           // set by the launcher: tag bits of the 16-bit-tag hash (-1: 32-bit id slots)
+  uint32_t hmul, hmaskb;  // 16-bit-tag hash: odd multiplier and 2^B - 1 (2^B >= n)
   int32_t fp32;           // 1: FP32 baseline traversal (exact distances, no quantizer / re-rank)
   int32_t staged;         // set by the launcher: wide code rows gathered through a TMA stage
   uint32_t* vbm;          // visited_bits = -2: per-warp-slot visited bitmaps (workspace), else null

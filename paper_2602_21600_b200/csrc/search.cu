@@ -86,6 +86,9 @@ namespace {
 #ifndef AQR_HASH_DIRECT
 #define AQR_HASH_DIRECT 1  // 1: the shared-memory visited set is direct-mapped (0: 8-probe open addressing)
 #endif
+#ifndef AQR_HASH_TAG16
+#define AQR_HASH_TAG16 1  // 1: the direct-mapped visited set stores 16-bit tags of a bijective hash (half the bytes per slot)
+#endif
 #ifndef AQR_VBM_HINT
 #define AQR_VBM_HINT 1  // 1: visited-bitmap atomics carry an L2 evict-last policy
 #endif
@@ -325,6 +328,21 @@ __host__ __device__ constexpr bool nd_alias() {
   return !INL && !FP && AQR_FUSED_FILTER && LPR < 32;
 }
 
+// the visited hash's slot format for this index (see visit_new16): 16-bit tags when the id range
+// [0, 2^B), 2^B >= n, splits into hbits slot bits and at most 15 tag bits, else 32-bit ids
+void hash_params(const IndexView& ix, SearchCfg& c) {
+  c.htag = -1;
+  c.hmul = c.hmaskb = 0u;
+  if (!AQR_HASH_TAG16 || !AQR_HASH_DIRECT || c.hbits <= 0) return;
+  int b = 0;
+  while (b < 31 && ((int64_t)1 << b) < ix.n) ++b;
+  if (b < c.hbits) b = c.hbits;
+  if (b - c.hbits > 15) return;
+  c.htag = b - c.hbits;
+  c.hmaskb = b >= 32 ? ~0u : ((1u << b) - 1u);
+  c.hmul = (uint32_t)(2654435769ull >> (32 - b)) | 1u;  // ~2^b / golden ratio, odd
+}
+
 Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   Layout L;
   int o = hot_bytes;
@@ -335,7 +353,7 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
   // INLINE block buffer (AQR traversal on an INLINE index), else the visited hash.  The FP32
   // traversal runs the GATHER kernel even on an INLINE index, so it needs the hash region
-  L.region = (ix.blk && !c.fp32) ? L.buf_bytes : (c.hbits > 0 ? (4 << c.hbits) : 0);
+  L.region = (ix.blk && !c.fp32) ? L.buf_bytes : (c.hbits > 0 ? ((c.htag >= 0 ? 2 : 4) << c.hbits) : 0);
   if (c.staged) {  // staged_dists: 2 x kStage wide rows
     const int st = 2 * kStage * ix.d_pad;
     if (st > L.region) L.region = st;
@@ -808,6 +826,19 @@ __device__ __forceinline__ bool visit_new(uint32_t* h, int hbits, int32_t u, int
   return true;
 }
 
+// direct-mapped visited set with 16-bit tags: x = (u * A) mod 2^B (A odd, 2^B >= n) is a bijection
+// on [0, 2^B); its top hbits bits pick the slot and the low htag (<= 15) bits are stored, so (slot,
+// tag) identifies u exactly -- a hit is never a false positive -- at half the bytes of an id slot
+// (twice the slots in the same shared memory).  Empty slots hold 0xFFFF (no tag reaches 2^15)
+__device__ __forceinline__ bool visit_new16(uint16_t* h, const SearchCfg& c, int32_t u) {
+  const uint32_t x = ((uint32_t)u * c.hmul) & c.hmaskb;
+  const uint32_t s = x >> c.htag;
+  const uint16_t t = (uint16_t)(x & ((1u << c.htag) - 1u));
+  if (h[s] == t) return false;
+  h[s] = t;
+  return true;
+}
+
 // gather row entries >= 0 of a -1 padded adjacency row into nb[] (compacted, order kept);
 // if `h` is non-null, only ids newly inserted in the visited hash are kept.
 __device__ __forceinline__ int gather_row(const int32_t* row, int cap, int32_t* nb, uint32_t* h, int hbits,
@@ -1253,8 +1284,9 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
       }
     } else {
       if (vhash) {
+        // empty: 0xFFFFFFFF (id slots) / 0xFFFF (16-bit tags)
         uint4* h4 = reinterpret_cast<uint4*>(hash);
-        const int nh4 = (1 << c.hbits) >> 2;
+        const int nh4 = ((c.htag >= 0 ? 2 : 4) << c.hbits) >> 4;
         for (int t = lane; t < nh4; t += 32) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
       }
       if (vbm) {
@@ -1265,7 +1297,10 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
       __syncwarp();
       if (lane == 0) {
         W[0] = qkey(dcur, cur);
-        if (vhash) visit_new(hash, c.hbits, cur, fails);
+        if (vhash) {
+          if (c.htag >= 0) visit_new16(reinterpret_cast<uint16_t*>(hash), c, cur);
+          else visit_new(hash, c.hbits, cur, fails);
+        }
         if (vbm) atomicOr(vbm + (cur >> 5), 1u << (cur & 31));
       }
     }
@@ -1408,7 +1443,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
             const int32_t u = arow[t];
             deg += __popc(__ballot_sync(kFull, u >= 0));
             bool keep = u >= 0;
-            if (keep && vhash) keep = visit_new(hash, c.hbits, u, fails);
+            if (keep && vhash)
+              keep = c.htag >= 0 ? visit_new16(reinterpret_cast<uint16_t*>(hash), c, u) : visit_new(hash, c.hbits, u, fails);
             const uint32_t mk = __ballot_sync(kFull, keep);
             AQR_ASSERT(!keep || m + __popc(mk & ((1u << lane) - 1u)) < H::NB);
             if (keep) nb[m + __popc(mk & ((1u << lane) - 1u))] = u;
@@ -1860,6 +1896,7 @@ cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, in
   };
   SearchCfg cc = c;
   cc.staged = 0;
+  hash_params(ix, cc);
   Layout L = make_layout(ix, cc, Hot<LPR, CPL, CAP, nd_alias<LPR, INL, FP>()>::bytes);
   if (L.per_warp > 12 * 1024) wpb = 1;  // large per-warp state: pack the SMs warp by warp
   int per_sm = 0;
@@ -1867,7 +1904,7 @@ cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, in
   if (e != cudaSuccess) return e;
   if (!INL && !FP && LPR == 32) {
     // wide code rows: stage them by TMA unless the stage costs concurrently running queries
-    SearchCfg cs = c;
+    SearchCfg cs = cc;
     cs.staged = 1;
     const Layout Ls = make_layout(ix, cs, Hot<LPR, CPL, CAP, nd_alias<LPR, INL, FP>()>::bytes);
     const int ws = Ls.per_warp > 12 * 1024 ? 1 : wpb;
@@ -1957,7 +1994,9 @@ int hot_bytes(const IndexView& ix, bool fp) {
 size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int wpb) {
   const int hb = hot_bytes(ix, c.fp32 != 0);
   if (hb < 0) return ~(size_t)0;
-  return (size_t)make_layout(ix, c, hb).per_warp * wpb;
+  SearchCfg cc = c;
+  hash_params(ix, cc);
+  return (size_t)make_layout(ix, cc, hb).per_warp * wpb;
 }
 
 cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
