@@ -281,6 +281,7 @@ struct Layout {
   // runtime part of the per-warp layout; the hot arrays of the beam (Hot<> below) sit at
   // compile-time offsets before W, so every access to them is [warp base + immediate]
   int o_w, o_qc, o_qf, o_h, o_s23, per_warp;
+  int o_stg;      // staged wide-row gather: its 2 x kStage row buffer (after the visited hash)
   int q_alias;    // 1: query codes / fp32 query live in the hot arrays (rebuilt for Stage 2)
   int region;     // bytes of the hash / block-buffer region (reused by Stage 2/3)
   int buf_bytes;  // INLINE: one staged block (128-byte aligned)
@@ -353,9 +354,12 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   L.buf_bytes = (ix.blk_bytes + 127) & ~127;
   // INLINE block buffer (AQR traversal on an INLINE index), else the visited hash.  The FP32
   // traversal runs the GATHER kernel even on an INLINE index, so it needs the hash region
-  L.region = (ix.blk && !c.fp32) ? L.buf_bytes : (c.hbits > 0 ? ((c.htag >= 0 ? 2 : 4) << c.hbits) : 0);
-  if (c.staged) {  // staged_dists: 2 x kStage wide rows
-    const int st = 2 * kStage * ix.d_pad;
+  const int hbytes = c.hbits > 0 ? ((c.htag >= 0 ? 2 : 4) << c.hbits) : 0;
+  L.region = (ix.blk && !c.fp32) ? L.buf_bytes : hbytes;
+  int stg_rel = 0;
+  if (c.staged) {  // staged_dists: 2 x kStage wide rows, after the visited hash (both live in the beam)
+    stg_rel = (hbytes + 127) & ~127;
+    const int st = stg_rel + 2 * kStage * ix.d_pad;
     if (st > L.region) L.region = st;
   }
   // ... or the staged gather's buffer (wide rows: the query is too big for the hot arrays)
@@ -369,6 +373,7 @@ Layout make_layout(const IndexView& ix, const SearchCfg& c, int hot_bytes) {
   }
   o = (o + 127) & ~127;
   L.o_h = o; o += al16(L.region);
+  L.o_stg = L.o_h + stg_rel;
   if (in_hot) {
     L.o_qf = 0;
     L.o_qc = al16(4 * ix.d4);
@@ -1180,6 +1185,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
   int32_t* clb = reinterpret_cast<int32_t*>(wb + H::o_lb);
   int32_t* scnt = reinterpret_cast<int32_t*>(wb + H::o_cnt);
   uint8_t* blkbuf = wb + L.o_h;
+  uint8_t* stgbuf = wb + L.o_stg;  // the staged gather's rows (never overlaps the visited hash)
   uint32_t* vhash = c.hbits > 0 ? hash : nullptr;
   // visited_bits = -2: this warp slot's bitmap in global memory (exact; no shared memory)
   uint32_t* vbm = (!INL && c.vbm) ? c.vbm + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * c.vbm_words
@@ -1238,7 +1244,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
     // distance keys of a list of node ids: d^q (the method) or the fp32 baseline's exact distance
     auto dists = [&](const int32_t* ids_, int m_, int32_t* out_) {
       if (FP) fp_dists<LPR>(ix, qf, ids_, m_, out_, lane);
-      else if (LPR == 32 && STG) staged_dists<CPL>(ix, qreg, qq, ids_, m_, out_, lane, blkbuf, bar, sph);
+      else if (LPR == 32 && STG) staged_dists<CPL>(ix, qreg, qq, ids_, m_, out_, lane, stgbuf, bar, sph);
       else list_dists<LPR, CPL>(ix, qreg, qq, ids_, m_, out_, lane);
     };
 

@@ -48,8 +48,10 @@ def _parity(oix, ix, q, p, visited_bits=-1, ctx=""):
 
 
 @pytest.mark.parametrize("ef", [96, 256])
-@pytest.mark.parametrize("vb", [-1, -2])
+@pytest.mark.parametrize("vb", [-1, -2, 8, 12])
 def test_c4slice_wide_rows_cap160(ef, vb):
+    """The wide-row (TMA-staged) kernel with every visited mode; vb 8 / 12 put the shared-memory
+    hash beside the stage buffer (they once shared one region: staged rows overwrote the table)."""
     c = case("c4slice")
     assert c.graph.M == 35 and c.w.x.shape[1] == 960
     ix = _upload(c)
@@ -61,8 +63,10 @@ def test_c4slice_wide_rows_cap160(ef, vb):
 
 
 @pytest.mark.parametrize("name", ["c1small", "c2slice"])
-@pytest.mark.parametrize("vb", [12, 13])
+@pytest.mark.parametrize("vb", [6, 10, 12, 13])
 def test_shared_memory_visited_hash(name, vb):
+    """The direct-mapped table (16-bit tags of a bijective hash, R15) at sizes from thrashing (2^6
+    slots: every slot rewritten many times per query) to roomy: results and visit order exact."""
     c = case(name)
     ix = _upload(c)
     p = dict(k=c.w.k, **oracle.ef_mapping(96, c.w.k))
