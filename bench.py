@@ -507,6 +507,7 @@ def run_aqr(args):
         log(f"[bench] visited_bits sweep {vb_results} -> {best_vb}")
     p = aqr.make_params(k, **m, visited_bits=best_vb, traversal=args.kt)
     s = aqr.Searcher(ix, len(q), p)
+    wpq_plan = aqr.search_plan(ix, len(q), p)  # 1: search_kernel (a warp per query), 4: coop_kernel
     # counters for the roofline (separate, untimed run with the stats path)
     s.totals.zero_()
     s.run(q, stats=True)
@@ -681,6 +682,7 @@ def run_aqr(args):
                        "recall@10": next((z["recall"] for z in sweep if z["ef"] == chosen and z["rerank"] == chosen_mode),
                                          None),
                        "visited_bits": best_vb, "visited_bits_sweep": vb_results, "queries_per_rank": len(q),
+                       "warps_per_query": wpq_plan,
                        "parallelism": f"replicated index, query-parallel over {world} GPU(s), no data-path collective",
                        "l2": "index (codes+adjacency+fp32) > 126 MB L2; no flush",
                        "pipeline": P, "pipeline_note": ("steps issued round-robin on this many CUDA streams, each "
@@ -695,7 +697,7 @@ def run_aqr(args):
                                      "profiles/r02/ncu_search_c2_head*.txt)"),
                          "bytes_per_query": round(bq, 1), "peak_source": peak_src,
                          "distinct_eval_ratio": round(ratio, 4), "distinct_ratio_sample": n_ratio,
-                         "kernel": "search_kernel", "kernel_ms": round(launch_ms, 4)},
+                         "kernel": "coop_kernel" if wpq_plan == 4 else "search_kernel", "kernel_ms": round(launch_ms, 4)},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_val, 1), "unit": "queries/s",
                     "h2d_bytes_per_step": h2d_all, "d2h_bytes_per_step": d2h_all,
@@ -928,7 +930,9 @@ def run_sharded(args):
             "config": {"workload": f"C5: {S} shards x {n_shard} x 96 l2, {nq} queries, k={k}", "ef": m["ef"],
                        "n_coarse": m["n_coarse"], "n_rerank": m["n_rerank"], "recall@10": round(r10, 4),
                        "recall@100": round(r100, 4), "parallelism": f"{S} shards over {world} GPU(s), NCCL all-gather + merge",
-                       "shards_per_rank": len(mine), "visited_bits": args.vbits[0], "l2": "shard indexes > 126 MB L2; no flush", "shards": infos},
+                       "shards_per_rank": len(mine), "visited_bits": args.vbits[0],
+                       "warps_per_query": aqr.search_plan(shards[0][1], nq, shards[0][2].params) if shards else None,
+                       "l2": "shard indexes > 126 MB L2; no flush", "shards": infos},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None, "bytes_per_query": round(bq_tot, 1),
                          "kernel": "search_kernel (all shards of rank 0)", "kernel_ms": round(kern_ms, 4),

@@ -168,6 +168,12 @@ typedef struct {
                            distances", R27): >= 0 re-ranks only the entries of A with
                            d^a <= (1 + tau_spread) d^a_k (at least k, at most n_rerank); +inf
                            (INFINITY) = the static n_rerank.  NaN or < 0: AQR_E_INVALID. */
+  int32_t warps_per_query; /* 0 = auto (default), 1 = one warp per query, 4 = one CTA of 4 warps per
+                           query: the warps split each expansion's visited test, code gathers,
+                           scoring, W dedupe and W insert (same results, visit order and counters).
+                           Auto picks 4 for GATHER-layout AQR searches whose one-warp launch holds
+                           <= 4 queries per SM (large ef: W alone fills the shared memory).  4 with the FP32 traversal or an INLINE index (AQR traversal):
+                           AQR_E_INVALID; other values: AQR_E_INVALID. */
 } aqr_search_params;
 
 enum { AQR_TRAVERSAL_AQR = 0, AQR_TRAVERSAL_FP32 = 1 };
@@ -203,10 +209,18 @@ size_t aqr_search_workspace_size(const aqr_index *ix, int64_t nq, const aqr_sear
 /* Search nq queries q (device [nq x ld_q] fp32).  Writes out_ids (device [nq x k] int32,
  * id_base + node id, -1 padding) and out_dist (device [nq x k] fp32: d^e for re-ranked
  * entries, d^a for entries filled from A; +inf padding), sorted by (dist, id).
- * One warp per query, persistent grid; asynchronous on `stream`. */
+ * One warp (or one CTA of 4 warps, warps_per_query) per query, persistent grid; asynchronous
+ * on `stream`. */
 aqr_status aqr_search(const aqr_index *ix, const float *q, int64_t nq, int64_t ld_q,
                       const aqr_search_params *p, int32_t *out_ids, float *out_dist,
                       const aqr_debug *debug, void *ws, size_t ws_bytes, aqr_stream_t stream);
+
+/* The launch aqr_search would make for these arguments, without launching: *warps_per_query =
+ * 1 (one warp per query) or 4 (one cooperative CTA of 4 warps per query), resolving
+ * p->warps_per_query = 0 (auto) by the rule above.  Host-only (an occupancy query on the current
+ * device); validation as aqr_search. */
+aqr_status aqr_search_plan(const aqr_index *ix, int64_t nq, const aqr_search_params *p,
+                           int32_t *warps_per_query);
 
 /* Stages 2 / ET / 3 / assembly alone (Alg2 l.8-24) on caller-supplied coarse lists:
  * cand_ids device [nq x n_cand] int32 node ids sorted by (d^q, id); a -1 ends a list early.

@@ -50,7 +50,7 @@ class SearchParams(C.Structure):
     _fields_ = [("k", C.c_int32), ("ef", C.c_int32), ("n_coarse", C.c_int32), ("n_rerank", C.c_int32),
                 ("tau_gap", C.c_double), ("tau_ratio", C.c_double), ("early_term", C.c_int32),
                 ("assemble_mode", C.c_int32), ("visited_bits", C.c_int32), ("warps_per_block", C.c_int32),
-                ("traversal", C.c_int32), ("tau_spread", C.c_double)]
+                ("traversal", C.c_int32), ("tau_spread", C.c_double), ("warps_per_query", C.c_int32)]
 
 
 class Debug(C.Structure):
@@ -63,7 +63,7 @@ class Debug(C.Structure):
 LAYOUTS = {"auto": 0, "gather": 1, "inline": 2}
 EXPORTS = ["aqr_encode", "aqr_upload_index", "aqr_index_free", "aqr_index_device_bytes", "aqr_index_layout",
            "aqr_search_workspace_size",
-           "aqr_search", "aqr_rerank", "aqr_merge_topk", "aqr_build_graph", "aqr_last_error", "aqr_version"]
+           "aqr_search", "aqr_search_plan", "aqr_rerank", "aqr_merge_topk", "aqr_build_graph", "aqr_last_error", "aqr_version"]
 
 _lib = None
 
@@ -255,8 +255,11 @@ TRAVERSALS = {"aqr": 0, "fp32": 1}
 
 
 def make_params(k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True, assemble_mode=0,
-                visited_bits=0, warps_per_block=0, traversal="aqr", tau_spread=math.inf) -> SearchParams:
+                visited_bits=0, warps_per_block=0, traversal="aqr", tau_spread=math.inf,
+                warps_per_query=0) -> SearchParams:
+    """warps_per_query: 0 auto, 1 one warp per query, 4 one cooperative CTA of 4 warps (include/aqr.h)."""
     p = SearchParams()
+    p.warps_per_query = warps_per_query
     p.tau_spread = tau_spread
     p.traversal = TRAVERSALS[traversal]
     p.k, p.ef, p.n_coarse, p.n_rerank = k, ef, n_coarse, n_rerank
@@ -264,6 +267,13 @@ def make_params(k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.008, early
     p.early_term, p.assemble_mode = int(bool(early_term)), assemble_mode
     p.visited_bits, p.warps_per_block = visited_bits, warps_per_block
     return p
+
+
+def search_plan(index: Index, nq: int, params: SearchParams) -> int:
+    """Warps per query aqr_search would use for this launch (1 or 4; aqr_search_plan)."""
+    g = C.c_int32(0)
+    _check(lib().aqr_search_plan(index.handle, C.c_int64(nq), C.byref(params), C.byref(g)), "aqr_search_plan")
+    return int(g.value)
 
 
 class Searcher:
@@ -309,7 +319,7 @@ class Searcher:
 
 def search(index: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True,
            assemble_mode=0, visited_bits=0, warps_per_block=0, trace=False, exp_cap=4096, stream=None,
-           traversal="aqr", tau_spread=math.inf):
+           traversal="aqr", tau_spread=math.inf, warps_per_query=0):
     """aqr_search on q [nq, d] fp32 CUDA -> (ids [nq, k] int32, dist [nq, k] fp32[, trace dict])."""
     torch = _torch()
     pq = _dev(q, torch.float32, "q")
@@ -317,7 +327,7 @@ def search(index: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=
         raise AqrError(f"q must be [nq, {index.d}], got {tuple(q.shape)}")
     nq = q.shape[0]
     p = make_params(k, ef, n_coarse, n_rerank, tau_gap, tau_ratio, early_term, assemble_mode, visited_bits,
-                    warps_per_block, traversal, tau_spread)
+                    warps_per_block, traversal, tau_spread, warps_per_query)
     dev = q.device
     ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
     dist = torch.empty((nq, k), dtype=torch.float32, device=dev)

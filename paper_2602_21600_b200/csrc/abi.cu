@@ -345,6 +345,10 @@ static aqr_status check_search_params(const aqr_search_params* p, bool need_ef) 
   AQR_CHECK_ARG(p->warps_per_block >= 0 && p->warps_per_block <= 8, "search: warps_per_block must be in [0, 8]");
   AQR_CHECK_ARG(p->traversal == AQR_TRAVERSAL_AQR || p->traversal == AQR_TRAVERSAL_FP32,
                 "search: traversal must be AQR_TRAVERSAL_AQR (0) or AQR_TRAVERSAL_FP32 (1)");
+  AQR_CHECK_ARG(p->warps_per_query == 0 || p->warps_per_query == 1 || p->warps_per_query == 4,
+                "search: warps_per_query must be 0 (auto), 1 or 4");
+  AQR_CHECK_ARG(p->warps_per_query <= 1 || p->traversal == AQR_TRAVERSAL_AQR,
+                "search: warps_per_query 4 needs the AQR traversal");
   return AQR_OK;
 }
 
@@ -367,6 +371,7 @@ static aqr::SearchCfg make_cfg(const aqr_search_params* p) {
   c.vbm_slots = 0;
   c.fp32 = p->traversal == AQR_TRAVERSAL_FP32;
   c.staged = 0;  // chosen per launch by launch_search
+  c.wpq = p->warps_per_query;
   return c;
 }
 
@@ -388,6 +393,8 @@ aqr_status aqr_search(const aqr_index* ix, const float* q, int64_t nq, int64_t l
   AQR_CHECK_ARG(!(ix->layout == AQR_LAYOUT_INLINE && p->traversal == AQR_TRAVERSAL_AQR &&
                   (p->visited_bits == -2 || p->visited_bits > 0)),
                 "search: visited sets (visited_bits -2 or 6..16) need the GATHER layout");
+  AQR_CHECK_ARG(!(ix->layout == AQR_LAYOUT_INLINE && p->traversal == AQR_TRAVERSAL_AQR && p->warps_per_query == 4),
+                "search: warps_per_query 4 needs the GATHER layout");
   aqr::SearchCfg c = make_cfg(p);
 #ifndef AQR_WARPS_PER_CTA
 #define AQR_WARPS_PER_CTA 4
@@ -409,6 +416,19 @@ aqr_status aqr_search(const aqr_index* ix, const float* q, int64_t nq, int64_t l
   AQR_CUDA(cudaMemsetAsync(ws, 0, 256, s), "search: memset");
   AQR_CUDA(aqr::launch_search(ix->v, c, q, nq, ld_q, out_ids, out_dist, debug, static_cast<int*>(ws), wpb, s),
            "search: kernel launch");
+  return AQR_OK;
+}
+
+aqr_status aqr_search_plan(const aqr_index* ix, int64_t nq, const aqr_search_params* p, int32_t* warps_per_query) {
+  aqr::g_err.clear();
+  AQR_CHECK_ARG(ix != nullptr && warps_per_query != nullptr, "search_plan: null pointer");
+  aqr_status st = check_search_params(p, true);
+  if (st != AQR_OK) return st;
+  AQR_CHECK_ARG(nq >= 0, "search_plan: nq < 0");
+  aqr::SearchCfg c = make_cfg(p);
+  int g = 1;
+  AQR_CUDA(aqr::plan_search(ix->v, c, nq, AQR_WARPS_PER_CTA, &g), "search_plan: occupancy query");
+  *warps_per_query = g;
   return AQR_OK;
 }
 

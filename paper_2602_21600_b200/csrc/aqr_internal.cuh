@@ -43,6 +43,7 @@ struct SearchCfg {
   uint32_t hmul, hmaskb;  // 16-bit-tag hash: odd multiplier and 2^B - 1 (2^B >= n)
   int32_t fp32;           // 1: FP32 baseline traversal (exact distances, no quantizer / re-rank)
   int32_t staged;         // set by the launcher: wide code rows gathered through a TMA stage
+  int32_t wpq;            // warps per query: 0 auto, 1 one warp, 4 a cooperative CTA (coop_kernel)
   uint32_t* vbm;          // visited_bits = -2: per-warp-slot visited bitmaps (workspace), else null
   int64_t vbm_words;      // 32-bit words per bitmap (multiple of 4)
   int64_t vbm_slots;      // bitmaps available (bounds the persistent grid's warps)
@@ -70,6 +71,7 @@ cudaError_t launch_rerank(const IndexView& ix, const SearchCfg& c, const float* 
 cudaError_t launch_merge(const float* dist, const int32_t* ids, int32_t n_lists, int64_t nq, int32_t k,
                          float* out_dist, int32_t* out_ids, cudaStream_t s);
 size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int warps_per_block);
+cudaError_t plan_search(const IndexView& ix, const SearchCfg& c, int64_t nq, int warps_per_block, int* wpq);
 cudaError_t launch_build_inline(const IndexView& ix, uint8_t* blk, cudaStream_t s);
 cudaError_t launch_code_norms(const IndexView& ix, int32_t* out, cudaStream_t s);
 // GPU index build (build.cu): codes [n x d_pad32] (d_pad32 a multiple of 32, zero padded), their

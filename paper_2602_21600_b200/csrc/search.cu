@@ -505,13 +505,13 @@ __device__ __forceinline__ void store_rows(const int (&part)[U], int r0, int g, 
   }
 }
 
-template <int LPR, int CPL>
+template <int LPR, int CPL, int UU = 0>
 __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg)[CPL], int qq,
                                            const int32_t* ids, int m, int32_t* out, int lane) {
   constexpr int G = 32 / LPR;
   // all loads of a pass are issued before any is consumed: U rows per lane, G * U rows per pass,
   // so a typical layer-0 expansion (<= 64 rows of 128 B) costs ONE DRAM round trip
-  constexpr int U = rows_u<CPL, LPR>();
+  constexpr int U = UU > 0 ? UU : rows_u<CPL, LPR>();
   static_assert(U % 4 == 0, "U must be a multiple of 4");
   const int g = lane / LPR, sub = lane % LPR;
   const int nch = ix.d_pad >> 5;
@@ -585,12 +585,12 @@ __device__ __forceinline__ void list_dists(const IndexView& ix, const C32 (&qreg
 // is dropped by the `id >= 0` test; a lane whose chunk lies past the row's end re-reads the last
 // chunk, multiplied by the query's zero chunk.  Same integers as list_dists.
 // ------------------------------------------------------------------------------------
-template <int LPR, int CPL>
+template <int LPR, int CPL, int UU = 0>
 __device__ __forceinline__ int list_filter(const IndexView& ix, const C32 (&qreg)[CPL], int qq,
                                            const int32_t* ids, int m, const uint64_t* W, int size, int ef,
                                            uint64_t* cs, int lane) {
   constexpr int G = 32 / LPR;
-  constexpr int U = rows_u<CPL, LPR>();
+  constexpr int U = UU > 0 ? UU : rows_u<CPL, LPR>();
   constexpr int PER = U >= LPR ? U / LPR : 1;
   constexpr int REP = U >= LPR ? 1 : LPR / U;
   const int g = lane / LPR, sub = lane % LPR;
@@ -1795,6 +1795,480 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
   }
 }
 
+// ------------------------------------------------------------------------------------
+// Cooperative search (aqr_search_params.warps_per_query = G > 1): one CTA of G warps per query,
+// the same algorithm as search_kernel with the same results, visit order and counters (the
+// parity tests run both).  For launches the one-warp kernel leaves latency-bound: a large ef
+// (W alone limits an SM to a few queries: C3 ef 5888 -> 4 warps per SM) or few queries (C4:
+// 1,000).  Per layer-0 expansion the G warps split
+//   * the visited test of the row (one entry per thread) and its compaction (row order kept),
+//   * the code gathers + dp4a scoring + max-W filter (list_filter) and the W dedupe: rows are
+//     dealt round-robin, row r to warp r % G,
+//   * the W insert: new keys ranked by all threads, the moved entries split into G contiguous
+//     pieces (each warp saves its piece's bottom np entries -- the only ones the piece below can
+//     overwrite -- then, after one barrier, block-moves the rest top-first in place and writes the
+//     new keys whose insertion points lie in its piece);
+// each warp finds the next expansion itself (all read the same W), so the next row is requested
+// before the insert, as in search_kernel.  Warp 0 alone runs the greedy descent and Stages 2-3.
+// ------------------------------------------------------------------------------------
+#ifndef AQR_COOP_U
+#define AQR_COOP_U 4  // rows per lane per scoring pass in the cooperative kernel
+#endif
+
+struct CoopMisc {
+  long long qi;
+  unsigned long long cmin;
+  int np, cur;
+  unsigned dcur;
+  int wcnt[16];
+  int cnt[16];
+  uint64_t bar[2];
+};
+
+struct CoopLayout {
+  int o_w, o_nbw, nbw, o_sw, o_cand, o_clb, o_cs, o_slb, o_qc, o_qf, o_h, o_s23, bytes;
+};
+
+template <int LPR, int CPL>
+__host__ __device__ constexpr int coop_pass() {
+  return (32 / LPR) * AQR_COOP_U;
+}
+
+CoopLayout make_coop_layout(const IndexView& ix, const SearchCfg& c, int G, int cap, int pass) {
+  CoopLayout L;
+  int o = (int)((sizeof(CoopMisc) + 127) & ~(size_t)127);
+  L.o_w = o; o += al16(8 * (c.ef + 1));
+  const int per = (cap + G - 1) / G;
+  L.nbw = (per + pass - 1) / pass * pass;  // one warp's id list, whole scoring passes
+  if (L.nbw < 32) L.nbw = 32;
+  L.o_nbw = o; o += al16(4 * G * L.nbw);
+  L.o_sw = o; o += al16(8 * G * L.nbw);
+  // cand doubles as the greedy descent's id list (rows of M <= 80 ids, padded to a pass)
+  const int ncand = cap > 96 + pass ? cap : 96 + pass;
+  L.o_cand = o; o += al16(8 * ncand);
+  L.o_clb = o; o += al16(4 * cap);
+  L.o_cs = o; o += al16(8 * ncand);
+  L.o_slb = o; o += al16(4 * cap);
+  L.o_qc = o; o += al16(ix.d_pad);
+  L.o_qf = o; o += al16(4 * ix.d4);
+  o = (o + 127) & ~127;
+  L.o_h = o; o += c.hbits > 0 ? al16((c.htag >= 0 ? 2 : 4) << c.hbits) : 0;
+  L.o_s23 = o; o += c.ef >= 2 * c.n_coarse ? 0 : al16(8 * c.n_coarse);
+  L.bytes = (o + 127) & ~127;
+  return L;
+}
+
+#ifndef AQR_COOP_MIN_CTAS
+#define AQR_COOP_MIN_CTAS 5  // register budget of the cooperative kernel (4 warps: <= 102 registers)
+#endif
+
+template <int LPR, int CPL, int CAP, int G>
+__global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexView ix, SearchCfg c, CoopLayout L,
+                                                          const float* __restrict__ q, int64_t nq, int64_t ld_q,
+                                                          int32_t* __restrict__ out_ids, float* __restrict__ out_dist,
+                                                          aqr_debug dbg, int dbg_flags, int* __restrict__ counter) {
+  constexpr int T = 32 * G;
+  constexpr int RJ = (CAP + T - 1) / T;  // row entries per thread
+  constexpr int PASS = coop_pass<LPR, CPL>();
+  static_assert(RJ * G <= 16, "row slots");
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  CoopMisc* sm = reinterpret_cast<CoopMisc*>(smem);
+  uint64_t* W = reinterpret_cast<uint64_t*>(smem + L.o_w);
+  int32_t* nball = reinterpret_cast<int32_t*>(smem + L.o_nbw);
+  int32_t* nbw = nball + w * L.nbw;  // this warp's id list
+  uint64_t* sw = reinterpret_cast<uint64_t*>(smem + L.o_sw) + w * L.nbw;
+  uint64_t* cand = reinterpret_cast<uint64_t*>(smem + L.o_cand);
+  int32_t* clb = reinterpret_cast<int32_t*>(smem + L.o_clb);
+  uint64_t* cs = reinterpret_cast<uint64_t*>(smem + L.o_cs);
+  int32_t* slb = reinterpret_cast<int32_t*>(smem + L.o_slb);
+  uint8_t* qc = smem + L.o_qc;
+  float* qf = reinterpret_cast<float*>(smem + L.o_qf);
+  uint32_t* vhash = c.hbits > 0 ? reinterpret_cast<uint32_t*>(smem + L.o_h) : nullptr;
+  uint32_t* vbm = c.vbm ? c.vbm + (int64_t)blockIdx.x * c.vbm_words : nullptr;
+  const uint64_t vpol = vbm ? vbm_policy() : 0ull;
+  const bool nocomp = !vhash && !vbm;
+  const int sub = lane % LPR;
+  const int nch = ix.d_pad >> 5;
+  const int ef = c.ef;
+  const int has_dbg = dbg_flags & 1;
+  int32_t* cnt = has_dbg ? sm->cnt : nullptr;
+  // the id lists' slots past the row never get a row entry: -1 once (list_filter reads whole passes)
+  for (int i = tid; i < G * L.nbw; i += T) nball[i] = -1;
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) sm->qi = atomicAdd(counter, 1);
+    if (cnt && tid < 16) cnt[tid] = 0;
+    __syncthreads();
+    const int64_t qi = sm->qi;
+    if (qi >= nq) break;
+    if ((dbg_flags & 2) && tid == 0) dbg.t_ns[2 * qi] = globaltimer_ns();
+    int fails = 0;
+    // 1. the query (warp 0), the visited set's reset (all)
+    if (w == 0) load_query(ix, q, ld_q, qi, qf, qc, lane);
+    if (vhash) {
+      uint4* h4 = reinterpret_cast<uint4*>(vhash);
+      const int nh4 = ((c.htag >= 0 ? 2 : 4) << c.hbits) >> 4;
+      for (int t = tid; t < nh4; t += T) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    }
+    if (vbm) {
+      uint4* b4 = reinterpret_cast<uint4*>(vbm);
+      for (int64_t t = tid; t < (c.vbm_words >> 2); t += T) b4[t] = make_uint4(0, 0, 0, 0);
+      __threadfence_block();
+    }
+    __syncthreads();
+    C32 qreg[CPL];
+#pragma unroll
+    for (int t = 0; t < CPL; ++t) {
+      const int ch = sub + LPR * t;
+      qreg[t].a = ch < nch ? reinterpret_cast<const uint4*>(qc)[2 * ch] : make_uint4(0, 0, 0, 0);
+      qreg[t].b = ch < nch ? reinterpret_cast<const uint4*>(qc)[2 * ch + 1] : make_uint4(0, 0, 0, 0);
+    }
+    int qq = 0;
+    for (int j = lane; j < ix.d_pad; j += 32) qq += (int)qc[j] * (int)qc[j];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) qq += __shfl_xor_sync(kFull, qq, off);
+
+    // 2. greedy descent through the upper layers (warp 0, R8)
+    if (w == 0) {
+      int32_t* gnb = reinterpret_cast<int32_t*>(cand);
+      int32_t* gnd = reinterpret_cast<int32_t*>(cs);
+      for (int i = lane; i < 2 * (L.o_clb - L.o_cand) / 8; i += 32) gnb[i] = -1;
+      int32_t cur = ix.entry;
+      if (lane == 0) gnb[0] = cur;
+      __syncwarp();
+      list_dists<LPR, CPL, AQR_COOP_U>(ix, qreg, qq, gnb, 1, gnd, lane);
+      __syncwarp();
+      uint32_t dcur = (uint32_t)gnd[0];
+      if (cnt && lane == 0) cnt[5] += 1;
+      for (int lv = ix.max_level; lv >= 1; --lv) {
+        for (;;) {
+          __syncwarp();
+          const int32_t* row = ix.adj_up + (int64_t)(__ldg(ix.up_off + cur) + lv - 1) * ix.M;
+          int deg;
+          const int m = gather_row(row, ix.M, gnb, nullptr, 0, fails, deg, lane);
+          list_dists<LPR, CPL, AQR_COOP_U>(ix, qreg, qq, gnb, m, gnd, lane);
+          __syncwarp();
+          uint64_t best = qkey(dcur, cur);
+          for (int r = lane; r < m; r += 32) {
+            const uint64_t kk = qkey((uint32_t)gnd[r], gnb[r]);
+            best = kk < best ? kk : best;
+          }
+          best = warp_min_u64(best);
+          if (cnt && lane == 0) {
+            cnt[3] += 1;
+            cnt[4] += deg;
+            cnt[5] += m;
+          }
+          if (qkey_id(best) == cur) break;
+          cur = qkey_id(best);
+          dcur = qkey_d(best);
+        }
+      }
+      if (lane == 0) {
+        sm->cur = cur;
+        sm->dcur = dcur;
+        W[0] = qkey(dcur, cur);
+        sm->np = 0;
+        sm->cmin = ~0ull;
+        if (vhash) {
+          if (c.htag >= 0) visit_new16(reinterpret_cast<uint16_t*>(vhash), c, cur);
+          else visit_new(vhash, c.hbits, cur, fails);
+        }
+        if (vbm) atomicOr(vbm + (cur >> 5), 1u << (cur & 31));
+      }
+    }
+    __syncthreads();
+
+    // 3. layer-0 beam (flag form); row entry j of the node to expand is held by thread j % T
+    int32_t myrow[RJ];
+    {
+      const int64_t rb = (int64_t)sm->cur * ix.ld0;
+#pragma unroll
+      for (int r = 0; r < RJ; ++r) {
+        const int j = tid + T * r;
+        myrow[r] = j < ix.cap0 ? __ldg(ix.adj0 + rb + j) : -1;
+      }
+    }
+    int size = 1, cursor = 0, nexp = 0, npos = -1;
+    for (;;) {
+      // the smallest unexpanded entry of W (every warp: same W, same answer)
+      int pos = -1;
+      if (npos != -1) {
+        if (npos < 0) break;
+        pos = npos;
+      } else {
+        for (int bb = cursor; bb < size; bb += 32) {
+          const int i = bb + lane;
+          const uint32_t mk = __ballot_sync(kFull, i < size && !(W[i] & 1ull));
+          if (mk) {
+            pos = bb + __ffs(mk) - 1;
+            break;
+          }
+        }
+        if (pos < 0) break;
+      }
+      const uint64_t wk = W[pos];
+      const int32_t cnode = qkey_id(wk);
+      AQR_ASSERT(cnode >= 0 && cnode < ix.n && !(wk & 1ull));
+      if (has_dbg && tid == 0 && dbg.exp_ids && nexp < dbg.exp_cap) dbg.exp_ids[qi * dbg.exp_cap + nexp] = cnode;
+      ++nexp;
+      // the row: visited test + compaction (row order), dealt to the warps' lists (entry r -> warp r % G)
+      int m;
+      if (nocomp) {
+        m = ix.cap0;
+#pragma unroll
+        for (int r = 0; r < RJ; ++r) {
+          const int j = tid + T * r;
+          if (j < ix.cap0) nball[(j % G) * L.nbw + j / G] = myrow[r];
+          if (cnt) {
+            const uint32_t mk = __ballot_sync(kFull, j < ix.cap0 && myrow[r] >= 0);
+            if (lane == 0) {
+              atomicAdd(cnt + 1, __popc(mk));
+              atomicAdd(cnt + 2, __popc(mk));
+            }
+          }
+        }
+      } else {
+        bool keep[RJ];
+        uint32_t old[RJ];
+        if (vbm) {
+#pragma unroll
+          for (int r = 0; r < RJ; ++r) {
+            const int32_t u = myrow[r];
+            old[r] = u >= 0 ? vbm_test_set(vbm + (u >> 5), 1u << (u & 31), vpol) : ~0u;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < RJ; ++r) {
+          const int32_t u = myrow[r];
+          if (vbm) keep[r] = u >= 0 && !(old[r] & (1u << (u & 31)));
+          else keep[r] = u >= 0 && (c.htag >= 0 ? visit_new16(reinterpret_cast<uint16_t*>(vhash), c, u)
+                                                : visit_new(vhash, c.hbits, u, fails));
+          const uint32_t mk = __ballot_sync(kFull, keep[r]);
+          if (lane == 0) sm->wcnt[r * G + w] = __popc(mk);
+          if (cnt) {
+            const uint32_t md = __ballot_sync(kFull, u >= 0);
+            if (lane == 0) atomicAdd(cnt + 1, __popc(md));
+          }
+        }
+        __syncthreads();
+        int tot = 0, base[RJ];
+#pragma unroll
+        for (int r = 0; r < RJ; ++r) base[r] = 0;
+        for (int s = 0; s < RJ * G; ++s) {
+          const int v = sm->wcnt[s];
+#pragma unroll
+          for (int r = 0; r < RJ; ++r)
+            if (s < r * G + w) base[r] += v;
+          tot += v;
+        }
+        m = tot;
+#pragma unroll
+        for (int r = 0; r < RJ; ++r) {
+          const uint32_t mk = __ballot_sync(kFull, keep[r]);
+          if (keep[r]) {
+            const int rk = base[r] + __popc(mk & ((1u << lane) - 1u));
+            nball[(rk % G) * L.nbw + rk / G] = myrow[r];
+          }
+        }
+        if (cnt && tid == 0) atomicAdd(cnt + 2, m);
+      }
+      __syncthreads();
+      // scoring + max-W filter + W dedupe of this warp's rows (W is read-only until the insert)
+      const int mw = (m - w + G - 1) / G;
+      if (!nocomp) {
+        const int top = (mw + PASS - 1) / PASS * PASS;
+        for (int i = mw + lane; i < top; i += 32) nbw[i] = -1;
+        __syncwarp();
+      }
+      const int np0 = list_filter<LPR, CPL, AQR_COOP_U>(ix, qreg, qq, nbw, mw, W, size, ef, sw, lane);
+      __syncwarp();
+      uint64_t cminw = ~0ull;
+      int npw = 0;
+      for (int j0 = 0; j0 < np0; j0 += 32) {
+        const int j = j0 + lane;
+        bool ok = false;
+        uint64_t kk = 0;
+        int lb = 0;
+        if (j < np0) {
+          kk = sw[j];
+          lb = lower_bound_w(W, size, kk);
+          ok = !(lb < size && (W[lb] & ~1ull) == kk);
+        }
+        const uint32_t mk = __ballot_sync(kFull, ok);
+        const int n = __popc(mk);
+        int b0 = 0;
+        if (lane == 0 && n) b0 = atomicAdd(&sm->np, n);
+        b0 = __shfl_sync(kFull, b0, 0);
+        if (ok) {
+          const int jj = b0 + __popc(mk & ((1u << lane) - 1u));
+          AQR_ASSERT(jj < CAP);
+          cand[jj] = kk;
+          clb[jj] = lb;
+          cminw = kk < cminw ? kk : cminw;
+        }
+        npw += n;
+      }
+      cminw = warp_min_u64(cminw);
+      if (lane == 0 && cminw != ~0ull) atomicMin(&sm->cmin, (unsigned long long)cminw);
+      if (cnt && lane == 0) {
+        atomicAdd(cnt + 11, np0);
+        atomicAdd(cnt + 12, npw);
+      }
+      __syncthreads();
+      // the next expansion: min(first unexpanded entry after pos, smallest new key); its row is
+      // requested now so the load overlaps the insert
+      const int np = sm->np;
+      {
+        const uint64_t cmin = sm->cmin;
+        uint64_t kw = ~0ull;
+        int kwpos = -1;
+        for (int bb = pos + 1; bb < size; bb += 32) {
+          const int i = bb + lane;
+          const uint32_t mk = __ballot_sync(kFull, i < size && !(W[i] & 1ull));
+          if (mk) {
+            kwpos = bb + __ffs(mk) - 1;
+            kw = W[kwpos];
+            break;
+          }
+        }
+        const uint64_t nxt = kw < cmin ? kw : cmin;
+        npos = nxt == ~0ull ? -2 : (kw < cmin ? kwpos : -3);
+        if (nxt != ~0ull) {
+          const int64_t rb = (int64_t)qkey_id(nxt) * ix.ld0;
+#pragma unroll
+          for (int r = 0; r < RJ; ++r) {
+            const int j = tid + T * r;
+            myrow[r] = j < ix.cap0 ? ldg_first(ix.adj0 + rb + j) : -1;
+          }
+        }
+      }
+      __syncthreads();  // every warp has read W, np and cmin
+      if (tid == 0) {
+        W[pos] = wk | 1ull;
+        sm->np = 0;
+        sm->cmin = ~0ull;
+      }
+      if (np == 0) {
+        cursor = pos + 1;
+        __syncthreads();
+        continue;
+      }
+      // insert: rank the new keys (all threads), then move W top-down in rounds
+      for (int i = tid; i < np; i += T) {
+        const uint64_t kk = cand[i];
+        int r = 0;
+        for (int j = 0; j < np; ++j) r += cand[j] < kk;
+        cs[r] = kk;
+        slb[r] = clb[i];
+      }
+      __syncthreads();
+      const int first_ins = slb[0];
+      if (npos == -3) npos = first_ins;
+      {
+        // the moved old entries [first_ins, size) split into G contiguous pieces, one per warp; each
+        // warp first saves the bottom np entries of its piece (the stores of the piece below may land
+        // there: an entry moves up by at most np), then, after one barrier, moves the rest top-first
+        // in place by per-segment block moves (as search_kernel) and stores the saved entries
+        constexpr int SV = (CAP + 31) / 32;
+        const int per = (size - first_ins + G - 1) / G;
+        const int a0 = first_ins + w * per;
+        const int a1 = a0 + per < size ? a0 + per : size;
+        const int nsv = a1 - a0 < np ? (a1 - a0 > 0 ? a1 - a0 : 0) : np;
+        uint64_t svv[SV];
+        int svd[SV];
+#pragma unroll
+        for (int t = 0; t < SV; ++t) {
+          const int i = lane + 32 * t;
+          svd[t] = -1;
+          if (i < nsv) {
+            const int p = a0 + i;
+            svv[t] = W[p];
+            int a = 0, b = np;  // shift = #{j : slb[j] <= p}
+            while (a < b) {
+              const int mid = (a + b) >> 1;
+              if (slb[mid] <= p) a = mid + 1;
+              else b = mid;
+            }
+            if (p + a < ef) svd[t] = p + a;
+          }
+        }
+        __syncthreads();
+        const int base = a0 + nsv;
+        for (int j = np - 1; j >= 0; --j) {
+          const int seg_top = j == np - 1 ? size : slb[j + 1];
+          if (seg_top <= base) break;  // this segment and all below lie under the piece's moved part
+          const int sh = j + 1;
+          const int seg_lo = slb[j] > base ? slb[j] : base;
+          int hi = seg_top < a1 ? seg_top : a1;
+          if (hi > ef - sh) hi = ef - sh;
+          for (; hi - 128 >= seg_lo; hi -= 128) {
+            const uint64_t v3 = W[hi - 32 + lane], v2 = W[hi - 64 + lane], v1 = W[hi - 96 + lane],
+                           v0 = W[hi - 128 + lane];
+            __syncwarp();
+            W[hi - 32 + lane + sh] = v3;
+            W[hi - 64 + lane + sh] = v2;
+            W[hi - 96 + lane + sh] = v1;
+            W[hi - 128 + lane + sh] = v0;
+          }
+          for (; hi > seg_lo; hi -= 32) {
+            const int p = hi - 32 + lane;
+            const bool in = p >= seg_lo;
+            uint64_t v = 0;
+            if (in) v = W[p];
+            __syncwarp();
+            if (in) W[p + sh] = v;
+          }
+          __syncwarp();
+        }
+#pragma unroll
+        for (int t = 0; t < SV; ++t)
+          if (svd[t] >= 0) W[svd[t]] = svv[t];
+        // new key j goes to slb[j] + j, written by the warp whose piece holds its insertion point:
+        // that slot is either in the warp's own (already moved) piece or among the next piece's
+        // saved entries, so no other warp still has to read it
+        __syncwarp();
+        for (int j = lane; j < np; j += 32) {
+          int own = per > 0 ? (slb[j] - first_ins) / per : 0;
+          if (own > G - 1) own = G - 1;
+          if (own == w && slb[j] + j < ef) W[slb[j] + j] = cs[j];
+        }
+      }
+      size = size + np < ef ? size + np : ef;
+      cursor = first_ins < pos + 1 ? first_ins : pos + 1;
+      __syncthreads();
+    }
+    if (cnt && tid == 0) {
+      cnt[0] = nexp;
+      cnt[10] = fails;
+    }
+    // 4-7. Stage 2, early termination, Stage 3, assembly (warp 0)
+    const int nc = c.n_coarse < size ? c.n_coarse : size;
+    if (w == 0) {
+      if (has_dbg) {
+        for (int i = lane; i < c.n_coarse; i += 32) {
+          const uint64_t wkk = i < nc ? W[i] : 0;
+          if (dbg.coarse_ids) dbg.coarse_ids[qi * c.n_coarse + i] = i < nc ? qkey_id(wkk) : -1;
+          if (dbg.coarse_dq) dbg.coarse_dq[qi * c.n_coarse + i] = i < nc ? (int32_t)qkey_d(wkk) : -1;
+        }
+      }
+      uint64_t* akeys = ef >= 2 * nc ? W + nc : reinterpret_cast<uint64_t*>(smem + L.o_s23);
+      __syncwarp();
+      finish_query(ix, c, qf, nullptr, W, nc, akeys, W, qi, out_ids, out_dist, dbg, has_dbg != 0, lane, cnt);
+      if (has_dbg && lane == 0) {
+        if (dbg.counters)
+          for (int t = 0; t < AQR_NCOUNT; ++t) dbg.counters[qi * AQR_NCOUNT + t] = cnt[t];
+        if (dbg.totals)
+          for (int t = 0; t < AQR_NCOUNT; ++t)
+            atomicAdd(reinterpret_cast<unsigned long long*>(dbg.totals + t), (unsigned long long)cnt[t]);
+      }
+      if ((dbg_flags & 2) && lane == 0) dbg.t_ns[2 * qi + 1] = globaltimer_ns();
+    }
+  }
+}
+
 // r_j = RN(1 / scale_j) and a check, for every code a in [0, 255], that div_code reproduces the
 // IEEE quotient RN(a / scale_j) bit for bit (one thread per (j, a)); any mismatch sets *bad
 __global__ void decode_recip_kernel(const float* __restrict__ scale, int32_t d4, float* __restrict__ rscale,
@@ -1874,10 +2348,41 @@ __global__ void __launch_bounds__(128) rerank_kernel(IndexView ix, SearchCfg c, 
   finish_query(ix, cc, qf, cid, nullptr, nc, akeys, rkeys, qi, out_ids, out_dist, none, false, lane, nullptr);
 }
 
+template <int LPR, int CPL, int CAP, int G>
+cudaError_t launch_coop(const IndexView& ix, const SearchCfg& cc, const float* q, int64_t nq, int64_t ld_q,
+                        int32_t* out_ids, float* out_dist, const aqr_debug& d, int flags, int* counter, int nsm,
+                        cudaStream_t s) {
+  auto kern = coop_kernel<LPR, CPL, CAP, G>;
+  const CoopLayout L = make_coop_layout(ix, cc, G, CAP, coop_pass<LPR, CPL>());
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.bytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * G, L.bytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int64_t grid = (int64_t)nsm * per_sm;
+  if (nq < grid) grid = nq;
+  if (cc.vbm && grid > cc.vbm_slots) grid = cc.vbm_slots;  // one bitmap per CTA
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, 32 * G, L.bytes, s>>>(ix, cc, L, q, nq, ld_q, out_ids, out_dist, d, flags, counter);
+  return cudaGetLastError();
+}
+
+// warps per query (include/aqr.h): one CTA of 4 warps per query where W alone limits an SM to <= 4
+// one-warp queries (large ef: C3 at ef 5888, 165 -> 140 ms); measured no gain for C4's 1k queries
+// at ef 2480 (26.6 vs 27.3 ms: two dependent memory round trips per expansion dominate either way)
+// nor for C1's 100
+int choose_wpq(int requested, int resident_warps_per_sm) {
+  if (requested != 0) return requested;
+  return resident_warps_per_sm <= 4 ? 4 : 1;
+}
+
 template <int LPR, int CPL, bool INL, int CAP, bool FP = false>
 cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,
                      int32_t* out_ids, float* out_dist, const aqr_debug* dbg, int* counter, int wpb,
-                     cudaStream_t s) {
+                     cudaStream_t s, int* plan = nullptr) {
+  // plan != null: only report the warps per query this launch would use (no launch)
+  if (plan) *plan = 1;
   // the flags decide before anything else: a launch without trace / counters / timestamps runs
   // the instantiation compiled without debug code (GATHER AQR traversal; the others keep one)
   aqr_debug d{};
@@ -1928,6 +2433,19 @@ cudaError_t launch_t(const IndexView& ix, const SearchCfg& c, const float* q, in
   }
   e = resident(L, wpb, &per_sm);
   if (e != cudaSuccess) return e;
+  if (plan && (INL || FP)) return cudaSuccess;
+  if (!INL && !FP) {
+    const int G = choose_wpq(c.wpq, per_sm * wpb);
+    if (plan) {
+      *plan = G;
+      return cudaSuccess;
+    }
+    if (G == 4) {
+      SearchCfg ck = cc;
+      ck.staged = 0;
+      return launch_coop<LPR, CPL, CAP, 4>(ix, ck, q, nq, ld_q, out_ids, out_dist, d, flags, counter, nsm, s);
+    }
+  }
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const size_t smem = (size_t)L.per_warp * wpb;
   int64_t want = (nq + wpb - 1) / wpb;
@@ -2003,6 +2521,18 @@ size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int wpb) {
   SearchCfg cc = c;
   hash_params(ix, cc);
   return (size_t)make_layout(ix, cc, hb).per_warp * wpb;
+}
+
+cudaError_t plan_search(const IndexView& ix, const SearchCfg& c, int64_t nq, int wpb, int* wpq) {
+  *wpq = 1;
+  if (c.fp32) return cudaSuccess;
+  const bool inl = ix.blk != nullptr;
+#define AQR_PLAN(L_, C_, K_)                                                                                  \
+  return inl ? launch_t<L_, C_, true, K_>(ix, c, nullptr, nq, 0, nullptr, nullptr, nullptr, nullptr, wpb, 0, wpq) \
+             : launch_t<L_, C_, false, K_>(ix, c, nullptr, nq, 0, nullptr, nullptr, nullptr, nullptr, wpb, 0, wpq)
+  AQR_DISPATCH(shape_of(ix), AQR_PLAN)
+#undef AQR_PLAN
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_search(const IndexView& ix, const SearchCfg& c, const float* q, int64_t nq, int64_t ld_q,

@@ -31,12 +31,12 @@ def _upload(c, layout="gather"):
     return aqr.upload_index(codes, x, quant, c.graph, metric=c.w.metric, layout=layout)
 
 
-def _parity(oix, ix, q, p, visited_bits=-1, ctx=""):
+def _parity(oix, ix, q, p, visited_bits=-1, ctx="", **gkw):
     import torch
     import paper_2602_21600_b200 as aqr
     o_ids, o_d, o_tr = oracle.search(oix, q, trace=True, exp_cap=4096, **p)
     g_ids, g_d, g_tr = aqr.search(ix, torch.from_numpy(np.ascontiguousarray(q)).cuda(), trace=True, exp_cap=4096,
-                                  visited_bits=visited_bits, **p)
+                                  visited_bits=visited_bits, **p, **gkw)
     torch.cuda.synchronize()
     g_tr = {k: v.cpu().numpy() for k, v in g_tr.items()}
     np.testing.assert_array_equal(g_tr["exp_ids"], o_tr["exp_ids"], err_msg=f"{ctx} visit order")

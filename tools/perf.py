@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--layout", default="gather")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--vbits", type=int, default=0)
+    ap.add_argument("--wpq", default="0", help="warps_per_query values to time, e.g. 1,4")
     args = ap.parse_args()
     import torch
     import bench
@@ -59,9 +60,9 @@ def main():
         path = aqr.lib_path() if name == "default" else os.path.join(B.PKG, f"libaqr_{name}.so")
         aqr._lib = load(path)
         ix = aqr.upload_index(codes, x, quant, g, metric=w.metric, layout=args.layout)
-        for ef in [int(e) for e in args.ef.split(",")]:
+        for ef, wpq in [(int(e), int(g)) for e in args.ef.split(",") for g in args.wpq.split(",")]:
             m = aqr.ef_mapping(ef, w.k)
-            s = aqr.Searcher(ix, len(q), aqr.make_params(w.k, **m, visited_bits=args.vbits))
+            s = aqr.Searcher(ix, len(q), aqr.make_params(w.k, **m, visited_bits=args.vbits, warps_per_query=wpq))
             s.run(q)
             s.run(q)
             torch.cuda.synchronize()
@@ -79,7 +80,7 @@ def main():
                 ref_ids[ef] = ids
             ed = E.exact_dist(x, q, s.ids, w.metric).cpu().numpy()
             rec = E.recall(ids, gt_ids, ed, gt_d, w.k)[1]
-            r = dict(variant=name, ef=ef, ms=round(ms, 3), qps=round(len(q) / ms * 1e3, 1), recall=round(rec, 4),
+            r = dict(variant=name, ef=ef, wpq=wpq, ms=round(ms, 3), qps=round(len(q) / ms * 1e3, 1), recall=round(rec, 4),
                      layout=ix.layout)
             out.append(r)
             print(json.dumps(r), flush=True)
