@@ -2021,6 +2021,7 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
 #pragma unroll
         for (int r = 0; r < RJ; ++r) {
           const int j = tid + T * r;
+          AQR_ASSERT(j >= ix.cap0 || (j / G < L.nbw && myrow[r] < ix.n));
           if (j < ix.cap0) nball[(j % G) * L.nbw + j / G] = myrow[r];
           if (cnt) {
             const uint32_t mk = __ballot_sync(kFull, j < ix.cap0 && myrow[r] >= 0);
@@ -2070,6 +2071,7 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
           const uint32_t mk = __ballot_sync(kFull, keep[r]);
           if (keep[r]) {
             const int rk = base[r] + __popc(mk & ((1u << lane) - 1u));
+            AQR_ASSERT(rk < ix.cap0 && rk / G < L.nbw && myrow[r] < ix.n);
             nball[(rk % G) * L.nbw + rk / G] = myrow[r];
           }
         }
@@ -2193,6 +2195,7 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
               else b = mid;
             }
             if (p + a < ef) svd[t] = p + a;
+            AQR_ASSERT(p < size && a >= 1 && a <= np);
           }
         }
         __syncthreads();
@@ -2204,6 +2207,7 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
           const int seg_lo = slb[j] > base ? slb[j] : base;
           int hi = seg_top < a1 ? seg_top : a1;
           if (hi > ef - sh) hi = ef - sh;
+          AQR_ASSERT(seg_lo >= first_ins && (hi <= seg_lo || (hi <= size && hi + sh <= ef)));
           for (; hi - 128 >= seg_lo; hi -= 128) {
             const uint64_t v3 = W[hi - 32 + lane], v2 = W[hi - 64 + lane], v1 = W[hi - 96 + lane],
                            v0 = W[hi - 128 + lane];
@@ -2233,6 +2237,7 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
         for (int j = lane; j < np; j += 32) {
           int own = per > 0 ? (slb[j] - first_ins) / per : 0;
           if (own > G - 1) own = G - 1;
+          AQR_ASSERT(slb[j] >= first_ins && slb[j] <= size);
           if (own == w && slb[j] + j < ef) W[slb[j] + j] = cs[j];
         }
       }

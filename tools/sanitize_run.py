@@ -1,7 +1,7 @@
 """A short end-to-end run of every kernel behind include/aqr.h for compute-sanitizer:
 encode (training + pack), upload (GATHER and INLINE), search in each kernel configuration the tests
-cover (AQR / FP32 traversal, no visited set / shared-memory hash / global bitmap, 128-d and 960-d
-rows, union assembly), the split re-rank and the shard merge, on small seeded inputs.  Checks the
+cover (AQR / FP32 traversal, one warp or a cooperative CTA per query, no visited set / shared-memory
+hash / global bitmap, 128-d and 960-d rows, union assembly), the split re-rank and the shard merge, on small seeded inputs.  Checks the
 results against the oracle so a silent corruption fails the run.
 
   compute-sanitizer --tool memcheck python tools/sanitize_run.py
@@ -40,11 +40,13 @@ def run(name, layouts=("gather", "inline"), vbits=(-1, 12, -2), traversals=("aqr
             for vb in vbits:
                 if layout == "inline" and vb not in (0, -1) and tr == "aqr":
                     continue
-                ids, d, t = aqr.search(ix, qd, trace=True, visited_bits=vb, traversal=tr, **p)
-                torch.cuda.synchronize()
-                if tr == "aqr":
-                    assert np.array_equal(ids.cpu().numpy(), o_ids), (name, layout, vb)
-                n_runs += 1
+                # the cooperative kernel (4 warps per query) for AQR searches on the GATHER layout
+                for wpq in ((1, 4) if (tr == "aqr" and layout == "gather") else (1,)):
+                    ids, d, t = aqr.search(ix, qd, trace=True, visited_bits=vb, traversal=tr, warps_per_query=wpq, **p)
+                    torch.cuda.synchronize()
+                    if tr == "aqr":
+                        assert np.array_equal(ids.cpu().numpy(), o_ids), (name, layout, vb, wpq)
+                    n_runs += 1
         ids_u, _ = aqr.search(ix, qd, assemble_mode=1, **p)
         ids2, _ = aqr.rerank(ix, qd, t["coarse_ids"], k, p["n_rerank"])
         torch.cuda.synchronize()
