@@ -104,6 +104,10 @@ namespace {
 #ifndef AQR_MOVE32
 #define AQR_MOVE32 3  // W segments move top first: 3 = 128 per step while long, then 64 (2 = 64 only, 1 = 32, 0 = 128)
 #endif
+#ifndef AQR_FLAT_MERGE
+#define AQR_FLAT_MERGE 10  // > 0: the W insert takes one chunked pass when np * this > entries moved (0: off;
+                          // 10: C5 2.98 -> 2.86 ms, C2 9.64 -> 9.60; 40: C2 9.92)
+#endif
 #ifndef AQR_FUSED_FILTER
 #define AQR_FUSED_FILTER 1  // 1: layer-0 scoring and the max-W filter in one pass (list_filter)
 #endif
@@ -1642,7 +1646,34 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
         wstart -= np;
       }
       int seg_hi = head ? 0 : size;
-      for (int j = head ? -1 : np - 1; j >= 0; --j) {
+      bool flat = false;
+#if AQR_FLAT_MERGE
+      // many short segments (W still filling: ~40 new keys spread over a few hundred entries, ~30
+      // instructions of loop overhead per segment): one top-down pass of 32-entry chunks instead,
+      // each lane's shift = #{j : slb[j] <= p} by a binary search over the sorted slb
+      if (!head && np * AQR_FLAT_MERGE > size - first_ins) {
+        flat = true;
+        for (int hi = size; hi > first_ins; hi -= 32) {
+          const int p = hi - 32 + lane;
+          uint64_t v = 0;
+          int dst = -1;
+          if (p >= first_ins) {
+            v = W[p];
+            int a = 0, b = np;
+            while (a < b) {
+              const int mid = (a + b) >> 1;
+              if (slb[mid] <= p) a = mid + 1;
+              else b = mid;
+            }
+            if (p + a < ef) dst = p + a;
+          }
+          __syncwarp();
+          if (dst >= 0) W[dst] = v;
+          __syncwarp();
+        }
+      }
+#endif
+      for (int j = (head || flat) ? -1 : np - 1; j >= 0; --j) {
         const int sh = j + 1;
         const int seg_lo = slb[j];
         int hi = seg_hi < ef - sh ? seg_hi : ef - sh;
