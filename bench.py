@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -344,6 +345,21 @@ def bytes_per_query(tot, nq, d, k, distinct_ratio=1.0, traversal="aqr"):
     return b / nq
 
 
+def sector_bytes_per_query(tot, nq, d, k, distinct_ratio=1.0, traversal="aqr"):
+    """bytes_per_query at 32-byte sector granularity: each row read rounded up to
+    whole sectors (C3's 100-byte codes occupy 128 B); adjacency rows rounded at the mean degree."""
+    def sec(b):
+        return 32.0 * math.ceil(b / 32.0)
+    exp, deg, ev, uexp, udeg, uev, nc, depth, et, na, fails = [float(v) for v in tot[:11]]
+    adj = exp * sec(4 * (deg / max(exp, 1.0) + 1)) + uexp * sec(4 * (udeg / max(uexp, 1.0) + 1))
+    evals = (ev - fails) * distinct_ratio + uev
+    if traversal == "fp32":
+        b = sec(4 * d) * nq + adj + sec(4 * d) * evals + 8 * k * nq
+    else:
+        b = sec(4 * d) * nq + adj + sec(d) * (evals + nc) + sec(4 * d) * depth + 8 * k * nq
+    return b / nq
+
+
 def oracle_index(w, cfg, codes, g, delta_override=float("nan")):
     """The oracle trains its own quantizer and encodes the base itself (full-size parity check
     of aqr_encode: codes compared byte for byte), then searches the same graph."""
@@ -523,6 +539,7 @@ def run_aqr(args):
     if best_vb != -1 and best_vb != 0:
         ratio = 1.0  # a visited set: the kernel's evaluation count is already the distinct one
     bq = bytes_per_query(tot_counters, len(q), w.x.shape[1], k, ratio, args.kt)
+    bq_sector = sector_bytes_per_query(tot_counters, len(q), w.x.shape[1], k, ratio, args.kt)
 
     # ---- the search kernel alone: isolated launches on one stream, events around each (the
     # roofline's kernel time) ----
@@ -695,7 +712,8 @@ def run_aqr(args):
                          "limiter": ("below the HBM roofline the kernel is bound by per-warp dependent chains and "
                                      "issue (ncu: DRAM ~11% of peak, L2 hit ~78%, issue ~62% busy; "
                                      "profiles/r02/ncu_search_c2_head*.txt)"),
-                         "bytes_per_query": round(bq, 1), "peak_source": peak_src,
+                         "bytes_per_query": round(bq, 1), "sector_bytes_per_query": round(bq_sector, 1),
+                         "peak_source": peak_src,
                          "distinct_eval_ratio": round(ratio, 4), "distinct_ratio_sample": n_ratio,
                          "kernel": "coop_kernel" if wpq_plan == 4 else "search_kernel", "kernel_ms": round(launch_ms, 4)},
             "cpu_baseline": cpu,
