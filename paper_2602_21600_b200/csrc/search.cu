@@ -104,6 +104,14 @@ namespace {
 #ifndef AQR_MOVE32
 #define AQR_MOVE32 3  // W segments move top first: 3 = 128 per step while long, then 64 (2 = 64 only, 1 = 32, 0 = 128)
 #endif
+#ifndef AQR_KW_HINT
+#define AQR_KW_HINT 1024  // ef >= this: after a new key is expanded next, the first unexpanded entry
+                          // after it is known from the insert (no scan over the expanded entries in
+                          // between): C3 ef 5888 -4.3% (cooperative kernel); see AQR_KW_HINT_SINGLE (0: off)
+#endif
+#ifndef AQR_KW_HINT_SINGLE
+#define AQR_KW_HINT_SINGLE 0  // 1: AQR_KW_HINT in the one-warp kernel too
+#endif
 #ifndef AQR_FLAT_MERGE
 #define AQR_FLAT_MERGE 10  // > 0: the W insert takes one chunked pass when np * this > entries moved (0: off;
                           // 10: C5 2.98 -> 2.86 ms, C2 9.64 -> 9.60; 40: C2 9.92)
@@ -889,6 +897,23 @@ __device__ __forceinline__ uint32_t vbm_test_set(uint32_t* w, uint32_t bit, uint
 #endif
 }
 
+// AQR_KW_HINT: position, after an insert of np sorted keys at insertion points slb[], of the first
+// unexpanded W entry after new key 0, given that the old entries from slb[0] up to the old
+// position kwpos (-1: none) are all expanded: min(new key 1 at slb[1] + 1, kwpos + #{j : slb[j] <=
+// kwpos}); -2 when neither is inside the list after the insert (warp-uniform)
+__device__ __forceinline__ int kw_hint(const int32_t* slb, int np, int kwpos, int size, int ef, int lane) {
+  int h = np > 1 ? slb[1] + 1 : INT_MAX;
+  if (kwpos >= 0) {
+    int sft = 0;
+    for (int j = lane; j < np; j += 32) sft += slb[j] <= kwpos;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) sft += __shfl_xor_sync(kFull, sft, off);
+    if (kwpos + sft < h) h = kwpos + sft;
+  }
+  const int nsize = size + np < ef ? size + np : ef;
+  return h < nsize ? h : -2;
+}
+
 // rank sort of n 64-bit distinct keys: dst[rank(src[i])] = src[i]
 __device__ __forceinline__ void rank_sort(const uint64_t* src, uint64_t* dst, int n, int lane) {
   for (int i = lane; i < n; i += 32) {
@@ -1338,6 +1363,13 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
     // AQR_KNOWN_NEXT: the position of the next expansion, known from the previous one (-1: scan
     // from the cursor, -2: W has no unexpanded entry left)
     int npos = -1;
+    // AQR_KW_HINT: the first unexpanded W entry after the next expansion, when the insert told it
+    // (-1: scan for it, -2: there is none).  Off in the one-warp kernel by default: in the
+    // 128-byte-row kernels the extra live state cost C2 1.3% even when unused, and C4 (wide rows,
+    // ef 2480) measured within its run-to-run noise (26.4-27.3 vs 26.4-27.1 ms); the cooperative
+    // kernel keeps it (C3 ef 5888: 142.3 -> 136.1 ms)
+    constexpr bool HINT = AQR_KW_HINT_SINGLE && AQR_KW_HINT > 0 && AQR_W_SLACK == 0 && !INL;
+    int khint = -1, kwpos_l = -1;
     for (;;) {
       // smallest unexpanded entry of W
       int pos = -1, gpos = -1;
@@ -1525,6 +1557,12 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
         cmin = warp_min_u64(cmin);
         uint64_t kw = ~0ull;
         int kwpos = -1;
+        if (HINT && khint != -1) {
+          if (khint >= 0) {
+            kwpos = khint;
+            kw = W[khint];
+          }
+        } else
         for (int bb = pos + 1; bb < size; bb += 32) {
           const int i = bb + lane;
           const bool un = i < size && !(W[i] & 1ull);
@@ -1535,6 +1573,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
             break;
           }
         }
+        khint = -1;
+        kwpos_l = kwpos;
         const uint64_t nxt = kw < cmin ? kw : cmin;
         // where the next expansion will sit after this one's merge: an old entry keeps its
         // position (every new key is larger than it), the smallest new key lands at its
@@ -1591,7 +1631,13 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
       }
       __syncwarp();
       const int first_ins = slb[0];
-      if (npos == -3) npos = first_ins;
+      if (npos == -3) {
+        npos = first_ins;
+        // the new key 0 is expanded next; every old entry in [slb[0], kwpos) is already expanded
+        // (pos was the smallest unexpanded, kwpos the first one after it), so the first unexpanded
+        // entry after it is new key 1 (at slb[1] + 1) or the old kwpos entry, shifted by the insert
+        if (HINT && ef >= AQR_KW_HINT) khint = kw_hint(slb, np, kwpos_l, size, ef, lane);
+      }
       // move whichever side of the insertion points is shorter: the entries after the first
       // one right (tail), or those before the last one left into the free head slots (head)
       bool head = AQR_W_SLACK > 0 && slb[np - 1] < size - first_ins && np <= AQR_W_SLACK;
@@ -1848,8 +1894,8 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
 
 struct CoopMisc {
   long long qi;
-  unsigned long long cmin;
-  int np, cur;
+  unsigned long long cmin[2];  // by expansion parity: one is filled while the other is reset
+  int np[2], cur;
   unsigned dcur;
   int wcnt[16];
   int cnt[16];
@@ -2001,8 +2047,8 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
         sm->cur = cur;
         sm->dcur = dcur;
         W[0] = qkey(dcur, cur);
-        sm->np = 0;
-        sm->cmin = ~0ull;
+        sm->np[0] = sm->np[1] = 0;
+        sm->cmin[0] = sm->cmin[1] = ~0ull;
         if (vhash) {
           if (c.htag >= 0) visit_new16(reinterpret_cast<uint16_t*>(vhash), c, cur);
           else visit_new(vhash, c.hbits, cur, fails);
@@ -2023,6 +2069,7 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
       }
     }
     int size = 1, cursor = 0, nexp = 0, npos = -1;
+    int khint = -1, kwpos_l = -1;  // AQR_KW_HINT (as in search_kernel)
     for (;;) {
       // the smallest unexpanded entry of W (every warp: same W, same answer)
       int pos = -1;
@@ -2044,6 +2091,7 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
       const int32_t cnode = qkey_id(wk);
       AQR_ASSERT(cnode >= 0 && cnode < ix.n && !(wk & 1ull));
       if (has_dbg && tid == 0 && dbg.exp_ids && nexp < dbg.exp_cap) dbg.exp_ids[qi * dbg.exp_cap + nexp] = cnode;
+      const int par = nexp & 1;
       ++nexp;
       // the row: visited test + compaction (row order), dealt to the warps' lists (entry r -> warp r % G)
       int m;
@@ -2133,7 +2181,7 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
         const uint32_t mk = __ballot_sync(kFull, ok);
         const int n = __popc(mk);
         int b0 = 0;
-        if (lane == 0 && n) b0 = atomicAdd(&sm->np, n);
+        if (lane == 0 && n) b0 = atomicAdd(&sm->np[par], n);
         b0 = __shfl_sync(kFull, b0, 0);
         if (ok) {
           const int jj = b0 + __popc(mk & ((1u << lane) - 1u));
@@ -2145,19 +2193,33 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
         npw += n;
       }
       cminw = warp_min_u64(cminw);
-      if (lane == 0 && cminw != ~0ull) atomicMin(&sm->cmin, (unsigned long long)cminw);
+      if (lane == 0 && cminw != ~0ull) atomicMin(&sm->cmin[par], (unsigned long long)cminw);
       if (cnt && lane == 0) {
         atomicAdd(cnt + 11, np0);
         atomicAdd(cnt + 12, npw);
       }
       __syncthreads();
+      // np / cmin of this expansion are complete; the other parity's pair is reset for the next
+      // one (everyone read it before this expansion's first barrier).  W[pos]'s flag: nothing
+      // reads it before the insert's barrier (the scans start at pos + 1, the dedupe masks it)
+      if (tid == 0) {
+        W[pos] = wk | 1ull;
+        sm->np[par ^ 1] = 0;
+        sm->cmin[par ^ 1] = ~0ull;
+      }
       // the next expansion: min(first unexpanded entry after pos, smallest new key); its row is
       // requested now so the load overlaps the insert
-      const int np = sm->np;
+      const int np = sm->np[par];
       {
-        const uint64_t cmin = sm->cmin;
+        const uint64_t cmin = sm->cmin[par];
         uint64_t kw = ~0ull;
         int kwpos = -1;
+        if (AQR_KW_HINT && khint != -1) {
+          if (khint >= 0) {
+            kwpos = khint;
+            kw = W[khint];
+          }
+        } else
         for (int bb = pos + 1; bb < size; bb += 32) {
           const int i = bb + lane;
           const uint32_t mk = __ballot_sync(kFull, i < size && !(W[i] & 1ull));
@@ -2167,6 +2229,8 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
             break;
           }
         }
+        khint = -1;
+        kwpos_l = kwpos;
         const uint64_t nxt = kw < cmin ? kw : cmin;
         npos = nxt == ~0ull ? -2 : (kw < cmin ? kwpos : -3);
         if (nxt != ~0ull) {
@@ -2178,15 +2242,9 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
           }
         }
       }
-      __syncthreads();  // every warp has read W, np and cmin
-      if (tid == 0) {
-        W[pos] = wk | 1ull;
-        sm->np = 0;
-        sm->cmin = ~0ull;
-      }
       if (np == 0) {
+        // no insert: W is unchanged (but for the flag), so the next expansion may start at once
         cursor = pos + 1;
-        __syncthreads();
         continue;
       }
       // insert: rank the new keys (all threads), then move W top-down in rounds
@@ -2199,7 +2257,10 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
       }
       __syncthreads();
       const int first_ins = slb[0];
-      if (npos == -3) npos = first_ins;
+      if (npos == -3) {
+        npos = first_ins;
+        if (AQR_KW_HINT && ef >= AQR_KW_HINT) khint = kw_hint(slb, np, kwpos_l, size, ef, lane);
+      }
       {
         // the moved old entries [first_ins, size) split into G contiguous pieces, one per warp; each
         // warp first saves the bottom np entries of its piece (the stores of the piece below may land
