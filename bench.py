@@ -36,9 +36,10 @@ EF_GRID = [16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512, 640, 768, 896, 1024,
 # fixed HNSW construction inputs of BASELINE.json
 P_MAX = {"C1": 0.2, "C2": 0.2, "C3": 0.0, "C4": 0.2, "C5": 5.0}
 TARGET_RECALL = 0.98
-# the ef our arm reports (smallest ef with recall@10 >= 0.98, measured, profiles/r01): the
-# reference arm (the oracle) is timed on the same point; configs without one use BJ's ef
-EF_AT_TARGET = {"C1": 64, "C2": 784, "C3": 1536, "C4": 128, "C5": 128}
+# the operating point our arm reports (smallest ef with recall@10 >= 0.98 and its re-rank mapping,
+# measured: profiles/r02/bench_c*.json): the reference arm (the oracle) is timed on the same point
+AT_TARGET = {"C1": (64, "exact"), "C2": (784, "preset"), "C3": (5888, "exact"), "C4": (2480, "full"),
+             "C5": (128, "preset")}
 LAYOUT = "auto"
 WJ_LITERAL = False  # --wj literal: Alg1 l.12 as printed (NEXT-4 variant; R16)
 BUILDER = "gpu"  # --builder: the index build on the GPU (aqr_build_graph) or the host builder
@@ -427,13 +428,9 @@ def run_aqr(args):
         # exactly (N_rerank = N_c) -- the Fig. 3 knob for data where d^q / d^a order is noisy (R20);
         # "exact": full with the early-termination thresholds at infinity (R26), so a
         # d^a gap can no longer cut the exact re-rank to k
-        mm = aqr.ef_mapping(ef, k)
         if args.traversal == "fp32":  # the baseline: W's first k are the result
             return dict(ef=max(ef, k), n_coarse=k, n_rerank=k)
-        if mode in ("full", "exact") or sq8:
-            mm["n_rerank"] = mm["n_coarse"]
-        if mode == "exact" or sq8:  # sq8: plain SQ8 HNSW (R23), every C entry re-ranked exactly
-            mm["early_term"] = False
+        mm = mode_mapping(aqr.ef_mapping, ef, k, mode, sq8)
         if args.tau_spread != float("inf") and not sq8:  # adaptive depth (NEXT-4, R27)
             mm["tau_spread"] = args.tau_spread
         return mm
@@ -972,6 +969,22 @@ def run_sharded(args):
 # --------------------------------------------------------------------------------------------
 # the reference arm: the CPU oracle as it stands (this tier has no reference implementation)
 # --------------------------------------------------------------------------------------------
+def mode_mapping(ef_mapping, ef, k, mode, sq8=False):
+    """Search parameters of a re-rank mapping at ef (both arms; `ef_mapping` is the binding's or the
+    oracle's copy of DESIGN.md R13).  "preset": Table 3 "0.97+" (R13); "full": the same N_c with every C
+    entry re-ranked exactly (N_rerank = N_c) -- the Fig. 3 knob for data where d^q / d^a order is noisy
+    (R20); "exact": full with the early-termination thresholds at infinity (R26), so a d^a gap can
+    no longer cut the exact re-rank to k.  "<mode>/<m>": the same with the EF multiplier m_ef = m
+    (ef_search = N_c x m_ef; Table 3 recommends 2-3; R29)."""
+    mode, _, mef = mode.partition("/")
+    mm = ef_mapping(ef, k, m_ef=int(mef) if mef else 3)
+    if mode in ("full", "exact") or sq8:
+        mm["n_rerank"] = mm["n_coarse"]
+    if mode == "exact" or sq8:  # sq8: plain SQ8 HNSW (R23), every C entry re-ranked exactly
+        mm["early_term"] = False
+    return mm
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -993,8 +1006,12 @@ def run_reference(args):
     g = G.build_hnsw(codes, M, efc, synth.level_draws(len(w.x), seed=w.seed, cfg=cfg), args.threads,
                      flags=BUILD_FLAGS)
     log(f"[reference] index built in {time.time() - t0:.1f} s")
-    ef = EF_AT_TARGET.get(cfg, 256) if args.ef == "auto" else int(args.ef)
-    m = G_ef_mapping(ef, k)
+    ef, mode = AT_TARGET.get(cfg, (256, "preset"))
+    if args.ef != "auto":
+        ef = int(args.ef)
+    if args.rerank not in ("auto", None) and "," not in args.rerank:
+        mode = args.rerank
+    m = mode_mapping(oracle.ef_mapping, ef, k, mode)
     oix = oracle.Index(w.x, codes, quant, g, w.metric)
     cores = os.cpu_count() or 1
     t0 = time.time()
@@ -1014,18 +1031,13 @@ def run_reference(args):
             "scaling": "strong" if cfg == "C5" else args.scaling,
             "vs_baseline": None, "dtype": "u8+int32+f32", "data": "synthetic",
             "config": {"workload": f"{cfg}: {len(w.x)} x {w.x.shape[1]} {w.metric}, {len(w.q)} queries, k={k}",
-                       "ef": ef, **m},
+                       "rerank": mode, **m},
             "cpu_baseline": {"value": round(v, 2), "unit": "queries/s", "cores": cores, "kind": "oracle",
                              "cpu_model": cpu_model(),
                              "sample": f"{per_step} queries per step (a bounded sample of the config's set), the "
                                        f"single-threaded C oracle run query-parallel on {cores} host threads"},
             "e2e": {"value": round(v, 2), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def G_ef_mapping(ef, k):
-    import oracle
-    return oracle.ef_mapping(ef, k)
 
 
 def main():
