@@ -2146,13 +2146,18 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
 #pragma unroll
           for (int r = 0; r < RJ; ++r) {
             const int32_t u = myrow[r];
-            old[r] = u >= 0 ? vbm_test_set(vbm + (u >> 5), 1u << (u & 31), vpol) : ~0u;
+            old[r] = u >= 0 ? (AQR_VBM_LOAD ? vbm_load(vbm + (u >> 5), vpol) : vbm_test_set(vbm + (u >> 5), 1u << (u & 31), vpol))
+                            : ~0u;
           }
         }
 #pragma unroll
         for (int r = 0; r < RJ; ++r) {
           const int32_t u = myrow[r];
-          if (vbm) keep[r] = u >= 0 && !(old[r] & (1u << (u & 31)));
+          if (vbm) {
+            // (AQR_VBM_LOAD: the CTA's threads test distinct ids of one row, so the load decides)
+            keep[r] = u >= 0 && !(old[r] & (1u << (u & 31)));
+            if (AQR_VBM_LOAD && keep[r]) vbm_set(vbm + (u >> 5), 1u << (u & 31), vpol);
+          }
           else keep[r] = u >= 0 && (c.htag >= 0 ? visit_new16(reinterpret_cast<uint16_t*>(vhash), c, u)
                                                 : visit_new(vhash, c.hbits, u, fails));
           const uint32_t mk = __ballot_sync(kFull, keep[r]);
