@@ -784,6 +784,40 @@ def cpu_baseline(w, oix, m, k, seconds, searcher, traversal="aqr"):
             "ids_equal_frac": round(float((a_ids == g_ids).all(1).mean()), 4)}
 
 
+def cpu_baseline_sharded(keep0, q_host, searcher0, m, k, n_shards, seconds):
+    """C5's cpu_baseline: the oracle as it stands on shard 0 (its own quantizer and codes, compared
+    byte for byte with aqr_encode's; the same graph), a bounded query sample on all host threads.
+    A CPU serving the whole job searches every shard, so the job-level value is the shard-0 rate
+    divided by the number of shards (the merge is negligible beside it)."""
+    import oracle
+    import torch
+    xs, samp, codes, g = keep0
+    t0 = time.time()
+    o_quant = oracle.train(xs, samp, p_max=P_MAX["C5"])
+    o_codes = oracle.encode(xs, o_quant)
+    codes_equal = bool(np.array_equal(o_codes, codes.cpu().numpy()))
+    oix = oracle.Index(xs, o_codes, o_quant, g, "l2")
+    prep = time.time() - t0
+    cores = os.cpu_count() or 1
+    t0 = time.time()
+    oracle.search(oix, q_host[:4], k, **m)
+    per_q = (time.time() - t0) / 4
+    n_a = int(max(cores, min(len(q_host), seconds * cores / max(per_q, 1e-6))))
+    t0 = time.time()
+    a_ids, _ = oracle_search_threads(oix, q_host[:n_a], k, cores, **m)
+    el = time.time() - t0
+    searcher0.run(torch.from_numpy(q_host).cuda())
+    torch.cuda.synchronize()
+    g_ids = searcher0.ids[:n_a].cpu().numpy()  # shard 0: id_base 0
+    return {"value": round(n_a / el / n_shards, 2), "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"shard 0 of {n_shards}, first {n_a} of {len(q_host)} queries, same graph/ef, the single-threaded C "
+                      f"oracle query-parallel on {cores} host threads ({el:.1f} s; training + encoding the shard "
+                      f"{prep:.1f} s, untimed); value = shard-0 rate {n_a / el:.1f} / {n_shards} shards",
+            "codes_equal_shard0": codes_equal,
+            "ids_equal_frac": round(float((a_ids == g_ids).all(1).mean()), 4)}
+
+
 # --------------------------------------------------------------------------------------------
 # C5: the base sharded 8 ways (SURVEY 8(e)); per-shard top-k merged locally, then over NCCL
 # --------------------------------------------------------------------------------------------
@@ -808,6 +842,7 @@ def run_sharded(args):
     threads = args.threads or max(1, (os.cpu_count() or 1) // min(world, 8))
     shards, infos = [], []
     gt_d_parts, gt_i_parts = [], []
+    keep0 = None
     for s_ in mine:
         t0 = time.time()
         xs = synth.gen_c5_shard(s_, n_shard)
@@ -832,6 +867,8 @@ def run_sharded(args):
                           build_s=round(time.time() - t0, 1), index_bytes=ix.device_bytes()))
         if rank == 0:
             log(f"[bench] C5 shard {s_}: {infos[-1]}")
+        if rank == 0 and s_ == 0 and not (args.no_cpu or args.no_oracle):
+            keep0 = (xs, samp, codes, g)  # shard 0's inputs for the cpu_baseline leg
 
     # the shards of a rank are searched concurrently on their own streams, so the persistent
     # grids of consecutive shards overlap instead of each launch paying its own tail
@@ -936,6 +973,10 @@ def run_sharded(args):
     a1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = allreduce_max(a0.elapsed_time(a1) / args.steps, world)
+    cpu = None
+    if rank == 0 and keep0 is not None:
+        cpu = cpu_baseline_sharded(keep0, q_host, shards[0][2], m, k, S, args.cpu_seconds)
+        log(f"[bench] C5 cpu_baseline {cpu}")
     if rank == 0:
         line = {
             "metric": "QPS (C5 sharded, recall@10 reported)", "value": round(value, 1), "unit": "queries/s",
@@ -954,7 +995,7 @@ def run_sharded(args):
                          "distinct_eval_ratio_per_shard": ratios,
                          "note": "bytes from kernel counters; distinct evaluations per shard measured with the exact "
                                  "visited bitmap (equal to the oracle's distinct count, test_gpu_visited)"},
-            "cpu_baseline": None,
+            "cpu_baseline": cpu,
             "e2e": {"value": round(nq / (e2e_ms / 1e3), 1), "unit": "queries/s", "h2d_bytes_per_step": int(q_host.nbytes),
                     "d2h_bytes_per_step": int(nq * k * 8)},
             "gpu_launches": args.steps * (len(shards) + (1 if len(shards) > 1 else 0) + (1 if world > 1 else 0)),
