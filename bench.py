@@ -874,7 +874,39 @@ def run_sharded(args):
     # grids of consecutive shards overlap instead of each launch paying its own tail
     side = [torch.cuda.Stream() for _ in shards] if args.shard_streams and len(shards) > 1 else None
 
+    # --exchange peer: no NCCL on the data path.  Rank r owns query block r; every (shard, owner)
+    # search writes its top-k straight into the owner's gather buffer (peer-mapped over NVLink),
+    # then signal / wait / one merge of all S lists of the own block (parallel.PeerExchange)
+    ex = None
+    if args.exchange == "peer":
+        ex = P.PeerExchange(aqr, nq, k, S)
+        blocks = [P.block_range(nq, world, o)[:2] for o in range(world)]
+        pstreams = [torch.cuda.Stream() for _ in range(min(8, len(shards) * world))]
+        psearch = [[aqr.Searcher(sh[1], max(ex.blk, 1), aqr.make_params(k, **m, visited_bits=args.vbits[0]))
+                    for _ in range(world)] for sh in shards]
+
+    def step_peer():
+        _, par = ex.begin()
+        main = torch.cuda.current_stream()
+        ready = torch.cuda.Event()
+        ready.record(main)
+        for st in pstreams:
+            st.wait_event(ready)
+        j = 0
+        for si, s_ in enumerate(mine):
+            for o, (lo, hi) in enumerate(blocks):
+                if hi > lo:
+                    psearch[si][o].run(q[lo:hi], stream=pstreams[j % len(pstreams)], out=ex.dest(o, s_, par))
+                    j += 1
+        for st in pstreams:
+            main.wait_stream(st)
+        ld, li = ex.finish(main)
+        md, mi = aqr.merge_topk(ld, li)
+        return md[: ex.hi - ex.lo], mi[: ex.hi - ex.lo]
+
     def step():
+        if ex is not None:
+            return step_peer()
         if side is None:
             outs = [sh[2].run(q) for sh in shards]
         else:
@@ -896,6 +928,18 @@ def run_sharded(args):
     # recall@10 / @100 against the merged exact ground truth (C5 is continuous: no exact ties)
     fd, fi = step()
     torch.cuda.synchronize()
+    if ex is not None:
+        ex.check()
+        fd, fi = P.gather_rows(fd), P.gather_rows(fi)  # reporting only: every rank's merged block
+        if args.check_exchange:
+            # the NCCL path on the same inputs must give the same lists
+            ex_keep, ex = ex, None
+            rd, ri = step()
+            ex = ex_keep
+            torch.cuda.synchronize()
+            same = bool(torch.equal(ri, fi) and torch.equal(rd, fd))
+            log(f"[bench] rank {rank}: peer exchange == NCCL all-gather + merge: {same}")
+            assert same, "peer exchange result differs from the NCCL path"
     gd_all = np.concatenate(gt_d_parts, 1)
     gi_all = np.concatenate(gt_i_parts, 1)
     if world > 1:
@@ -967,9 +1011,9 @@ def run_sharded(args):
     a0.record(stream)
     for _ in range(args.steps):
         q.copy_(qh, non_blocking=True)  # step() searches q
-        rd, ri = step()
-        ids_h.copy_(ri, non_blocking=True)
-        dist_h.copy_(rd, non_blocking=True)
+        rd, ri = step()  # peer exchange: this rank's merged block; NCCL path: all nq rows
+        ids_h[: ri.shape[0]].copy_(ri, non_blocking=True)
+        dist_h[: rd.shape[0]].copy_(rd, non_blocking=True)
     a1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = allreduce_max(a0.elapsed_time(a1) / args.steps, world)
@@ -985,7 +1029,11 @@ def run_sharded(args):
             "data": "synthetic (seeded, BASELINE.json configs[4] recipe)",
             "config": {"workload": f"C5: {S} shards x {n_shard} x 96 l2, {nq} queries, k={k}", "ef": m["ef"],
                        "n_coarse": m["n_coarse"], "n_rerank": m["n_rerank"], "recall@10": round(r10, 4),
-                       "recall@100": round(r100, 4), "parallelism": f"{S} shards over {world} GPU(s), NCCL all-gather + merge",
+                       "recall@100": round(r100, 4),
+                       "parallelism": (f"{S} shards over {world} GPU(s), NCCL all-gather + merge" if ex is None else
+                                       f"{S} shards over {world} GPU(s), peer-memory exchange (search epilogue stores "
+                                       f"into the block owner's buffer, signal/wait, one merge per block; no NCCL)"),
+                       "exchange": args.exchange,
                        "shards_per_rank": len(mine), "visited_bits": args.vbits[0],
                        "warps_per_query": aqr.search_plan(shards[0][1], nq, shards[0][2].params) if shards else None,
                        "l2": "shard indexes > 126 MB L2; no flush", "shards": infos},
@@ -998,10 +1046,15 @@ def run_sharded(args):
             "cpu_baseline": cpu,
             "e2e": {"value": round(nq / (e2e_ms / 1e3), 1), "unit": "queries/s", "h2d_bytes_per_step": int(q_host.nbytes),
                     "d2h_bytes_per_step": int(nq * k * 8)},
-            "gpu_launches": args.steps * (len(shards) + (1 if len(shards) > 1 else 0) + (1 if world > 1 else 0)),
+            "gpu_launches": args.steps * ((len(shards) + (1 if len(shards) > 1 else 0) + (1 if world > 1 else 0)) if ex is None
+                                          else (len(shards) * sum(1 for lo_, hi_ in blocks if hi_ > lo_) + 3)),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
+    if ex is not None:
+        torch.cuda.synchronize()
+        ex.check()
+        ex.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
@@ -1092,6 +1145,11 @@ def main():
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--ef", default="auto")
     ap.add_argument("--full-sweep", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="C5: how the per-shard top-k lists meet -- nccl: all_gather_into_tensor + merge (default); "
+                         "peer: aqr_search stores into the block owner's peer-mapped buffer, aqr_peer_signal / "
+                         "aqr_peer_wait, one merge per block (no NCCL on the data path)")
+    ap.add_argument("--check-exchange", action="store_true", help="C5 --exchange peer: assert the NCCL path gives the same lists")
     ap.add_argument("--shard-streams", type=int, default=1,
                     help="C5: search a rank's shards concurrently on separate CUDA streams (1) or one after another (0)")
     ap.add_argument("--stream", type=int, default=0,

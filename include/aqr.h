@@ -234,6 +234,43 @@ aqr_status aqr_rerank(const aqr_index *ix, const float *q, int64_t nq, int64_t l
 aqr_status aqr_merge_topk(const float *dist, const int32_t *ids, int32_t n_lists, int64_t nq,
                           int32_t k, float *out_dist, int32_t *out_ids, aqr_stream_t stream);
 
+/* ------------------------------------------------------------------------------------ */
+/* Peer-memory exchange for the sharded configuration (BASELINE.json configs[4]: "per-shard  */
+/* top-k gathered over NVLink and merged"; SURVEY 8(e) fused variant).  One process per GPU. */
+/* Each rank owns a block of the query batch.  A rank searches every query on its shard(s)    */
+/* with aqr_search, one launch per destination block, with out_ids / out_dist pointing INTO    */
+/* the owner's gather buffer (a peer-mapped pointer; the owner's own block is a local one):    */
+/* the search kernel's epilogue stores are the NVLink transfer.  Then aqr_peer_signal, on the  */
+/* owner aqr_peer_wait, and aqr_merge_topk over the [n_lists x blk x k] lists of its block.    */
+/* No NCCL call on the data path.                                                              */
+/* ------------------------------------------------------------------------------------ */
+#define AQR_MAX_PEERS 8
+#define AQR_PEER_HANDLE_BYTES 64
+
+/* cudaMalloc `bytes` (zero-filled) on the current device and export it: *dptr the local device
+ * pointer, handle[64] an IPC handle another process on this node opens with aqr_peer_open.
+ * Errors: AQR_E_INVALID, AQR_E_OOM, AQR_E_CUDA.  Free with aqr_peer_free (after every peer closed it). */
+aqr_status aqr_peer_alloc(size_t bytes, void **dptr, uint8_t *handle);
+/* Map a peer process's allocation (handle from ITS aqr_peer_alloc) into this process: *dptr is
+ * valid on the current device (peer access over NVLink is enabled by the mapping).  A process
+ * must not open its own handle (use the local pointer).  Unmap with aqr_peer_close. */
+aqr_status aqr_peer_open(const uint8_t *handle, void **dptr);
+aqr_status aqr_peer_close(void *dptr);
+aqr_status aqr_peer_free(void *dptr);
+/* After every kernel launched on `stream` so far: flags[i][slot] = value for i < n_peers, with
+ * system-scope release semantics (the stores those kernels made to peer memory are visible to a
+ * peer that acquires the flag).  flags: HOST array of n_peers DEVICE pointers (peer-mapped, or
+ * local for this rank's own) to uint64 arrays; 1 <= n_peers <= AQR_MAX_PEERS; value must grow
+ * from step to step.  Asynchronous. */
+aqr_status aqr_peer_signal(uint64_t *const *flags, int32_t n_peers, int32_t slot, uint64_t value,
+                           aqr_stream_t stream);
+/* Block `stream` (a spinning kernel, system-scope acquire loads) until flags[i] >= value for every
+ * i < n (flags: LOCAL device array, 1 <= n <= 32).  A flag still below value after timeout_ns
+ * makes the kernel give up and write 1 + i to *status (device int32, zeroed by the caller; may be
+ * NULL): the caller checks it after synchronizing.  Asynchronous. */
+aqr_status aqr_peer_wait(const uint64_t *flags, int32_t n, uint64_t value, uint64_t timeout_ns,
+                         int32_t *status, aqr_stream_t stream);
+
 /* Thread-local description of the last failure ("" if none). */
 const char *aqr_last_error(void);
 /* ------------------------------------------------------------------------------------ */

@@ -292,8 +292,10 @@ class Searcher:
         self._tdbg = None
         self.t_ns = None
 
-    def run(self, q, stream=None, stats=False, timing=False):
-        """timing=True: per-query [start, end] %globaltimer ns into self.t_ns [nq, 2] (no counters)."""
+    def run(self, q, stream=None, stats=False, timing=False, out=None):
+        """timing=True: per-query [start, end] %globaltimer ns into self.t_ns [nq, 2] (no counters).
+        out=(ids_ptr, dist_ptr): raw device addresses of [q.shape[0] x k] int32 / fp32 outputs written
+        instead of self.ids / self.dist (a peer GPU's gather buffer, PeerExchange.dest)."""
         torch = _torch()
         pq = _dev(q, torch.float32, "q")
         if q.dim() != 2 or q.shape[1] != self.index.d:
@@ -309,12 +311,12 @@ class Searcher:
                 self._tdbg = Debug()
                 self._tdbg.t_ns = self.t_ns.data_ptr()
             dbg = C.byref(self._tdbg)
+        o_ids, o_dist = (self.ids.data_ptr(), self.dist.data_ptr()) if out is None else (int(out[0]), int(out[1]))
         st = lib().aqr_search(self.index.handle, pq, C.c_int64(q.shape[0]), C.c_int64(q.shape[1]),
-                              C.byref(self.params), C.c_void_p(self.ids.data_ptr()),
-                              C.c_void_p(self.dist.data_ptr()), dbg,
+                              C.byref(self.params), C.c_void_p(o_ids), C.c_void_p(o_dist), dbg,
                               C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws.numel()), _stream(stream))
         _check(st, "aqr_search")
-        return self.ids, self.dist
+        return (self.ids, self.dist) if out is None else None
 
 
 def search(index: Index, q, k, ef, n_coarse, n_rerank, tau_gap=0.010, tau_ratio=1.008, early_term=True,
@@ -389,6 +391,71 @@ def merge_topk(dist, ids, k=None, stream=None):
                               C.c_void_p(oi.data_ptr()), _stream(stream))
     _check(st, "aqr_merge_topk")
     return od, oi
+
+
+# --------------------------------------------------------------------------------------
+# peer-memory exchange (include/aqr.h "Peer-memory exchange"; parallel.PeerExchange drives it)
+# --------------------------------------------------------------------------------------
+PEER_HANDLE_BYTES = 64
+MAX_PEERS = 8
+
+
+class PeerBuffer:
+    """Device memory from aqr_peer_alloc (owner) or a peer's allocation mapped by aqr_peer_open."""
+
+    def __init__(self, ptr: int, nbytes: int, owner: bool, handle: bytes = b""):
+        self.ptr, self.nbytes, self.owner, self.handle = ptr, nbytes, owner, handle
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr, False), "version": 2}
+
+    def tensor(self, dtype, shape, offset=0):
+        """A torch view of [offset, offset + prod(shape) x itemsize) -- LOCAL (owner) buffers only."""
+        torch = _torch()
+        if not self.owner:
+            raise AqrError("tensor views are for the local buffer; peers are addressed by pointer")
+        n = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+        if offset < 0 or offset + n > self.nbytes:
+            raise AqrError("view outside the buffer")
+        raw = torch.as_tensor(self, device="cuda")
+        return raw[offset:offset + n].view(dtype).view(*shape)
+
+    def close(self):
+        if self.ptr:
+            fn = lib().aqr_peer_free if self.owner else lib().aqr_peer_close
+            _check(fn(C.c_void_p(self.ptr)), "aqr_peer_free" if self.owner else "aqr_peer_close")
+            self.ptr = 0
+
+
+def peer_alloc(nbytes: int) -> PeerBuffer:
+    p = C.c_void_p()
+    h = (C.c_uint8 * PEER_HANDLE_BYTES)()
+    _check(lib().aqr_peer_alloc(C.c_size_t(nbytes), C.byref(p), h), "aqr_peer_alloc")
+    return PeerBuffer(int(p.value), nbytes, True, bytes(h))
+
+
+def peer_open(handle: bytes, nbytes: int) -> PeerBuffer:
+    if len(handle) != PEER_HANDLE_BYTES:
+        raise AqrError("bad peer handle")
+    p = C.c_void_p()
+    h = (C.c_uint8 * PEER_HANDLE_BYTES).from_buffer_copy(handle)
+    _check(lib().aqr_peer_open(h, C.byref(p)), "aqr_peer_open")
+    return PeerBuffer(int(p.value), nbytes, False)
+
+
+def peer_signal(flag_ptrs, slot: int, value: int, stream=None):
+    """aqr_peer_signal: flag_ptrs = device addresses (ints) of every rank's flag array."""
+    arr = (C.c_void_p * len(flag_ptrs))(*[C.c_void_p(int(v)) for v in flag_ptrs])
+    _check(lib().aqr_peer_signal(arr, C.c_int32(len(flag_ptrs)), C.c_int32(slot), C.c_uint64(value), _stream(stream)),
+           "aqr_peer_signal")
+
+
+def peer_wait(flags_ptr: int, n: int, value: int, timeout_ns: int, status=None, stream=None):
+    """aqr_peer_wait on the local flag array; status: a zeroed CUDA int32 tensor (or None)."""
+    sp = C.c_void_p(status.data_ptr()) if status is not None else C.c_void_p(0)
+    _check(lib().aqr_peer_wait(C.c_void_p(int(flags_ptr)), C.c_int32(n), C.c_uint64(value), C.c_uint64(timeout_ns), sp,
+                               _stream(stream)), "aqr_peer_wait")
 
 
 from .graph import Graph, build_hnsw, build_hnsw_gpu, adapt_params  # noqa: E402,F401

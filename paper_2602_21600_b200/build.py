@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_AQR = os.path.join(PKG, "libaqr.so")
 LIB_HNSW = os.path.join(PKG, "libaqr_hnsw.so")
-CU_SOURCES = ["encode.cu", "search.cu", "merge.cu", "build.cu", "abi.cu"]
+CU_SOURCES = ["encode.cu", "search.cu", "merge.cu", "peer.cu", "build.cu", "abi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v"]

@@ -528,4 +528,75 @@ aqr_status aqr_merge_topk(const float* dist, const int32_t* ids, int32_t n_lists
   return AQR_OK;
 }
 
+aqr_status aqr_peer_alloc(size_t bytes, void** dptr, uint8_t* handle) {
+  aqr::g_err.clear();
+  AQR_CHECK_ARG(bytes > 0 && dptr != nullptr && handle != nullptr, "peer_alloc: need bytes > 0 and non-null outputs");
+  static_assert(sizeof(cudaIpcMemHandle_t) == AQR_PEER_HANDLE_BYTES, "IPC handle size");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    set_error("aqr: peer_alloc: out of device memory");
+    return AQR_E_OOM;
+  }
+  AQR_CUDA(e, "peer_alloc: cudaMalloc");
+  e = cudaMemset(p, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_fail(e, "peer_alloc: memset / cudaIpcGetMemHandle");
+  }
+  memcpy(handle, &h, sizeof(h));
+  *dptr = p;
+  return AQR_OK;
+}
+
+aqr_status aqr_peer_open(const uint8_t* handle, void** dptr) {
+  aqr::g_err.clear();
+  AQR_CHECK_ARG(handle != nullptr && dptr != nullptr, "peer_open: null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  AQR_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "peer_open: cudaIpcOpenMemHandle");
+  *dptr = p;
+  return AQR_OK;
+}
+
+aqr_status aqr_peer_close(void* dptr) {
+  aqr::g_err.clear();
+  AQR_CHECK_ARG(dptr != nullptr, "peer_close: null pointer");
+  AQR_CUDA(cudaIpcCloseMemHandle(dptr), "peer_close: cudaIpcCloseMemHandle");
+  return AQR_OK;
+}
+
+aqr_status aqr_peer_free(void* dptr) {
+  aqr::g_err.clear();
+  AQR_CHECK_ARG(dptr != nullptr, "peer_free: null pointer");
+  AQR_CUDA(cudaFree(dptr), "peer_free: cudaFree");
+  return AQR_OK;
+}
+
+aqr_status aqr_peer_signal(uint64_t* const* flags, int32_t n_peers, int32_t slot, uint64_t value,
+                           aqr_stream_t stream) {
+  aqr::g_err.clear();
+  AQR_CHECK_ARG(flags != nullptr && n_peers >= 1 && n_peers <= AQR_MAX_PEERS, "peer_signal: need 1 <= n_peers <= 8");
+  AQR_CHECK_ARG(slot >= 0, "peer_signal: slot < 0");
+  for (int i = 0; i < n_peers; ++i) AQR_CHECK_ARG(flags[i] != nullptr, "peer_signal: null flag pointer");
+  AQR_CUDA(aqr::launch_peer_signal(reinterpret_cast<unsigned long long* const*>(flags), n_peers, slot,
+                                   (unsigned long long)value, reinterpret_cast<cudaStream_t>(stream)),
+           "peer_signal: kernel launch");
+  return AQR_OK;
+}
+
+aqr_status aqr_peer_wait(const uint64_t* flags, int32_t n, uint64_t value, uint64_t timeout_ns, int32_t* status,
+                         aqr_stream_t stream) {
+  aqr::g_err.clear();
+  AQR_CHECK_ARG(flags != nullptr && n >= 1 && n <= 32, "peer_wait: need 1 <= n <= 32");
+  AQR_CUDA(aqr::launch_peer_wait(reinterpret_cast<const unsigned long long*>(flags), n, (unsigned long long)value,
+                                 (unsigned long long)timeout_ns, status, reinterpret_cast<cudaStream_t>(stream)),
+           "peer_wait: kernel launch");
+  return AQR_OK;
+}
+
 }  // extern "C"

@@ -72,6 +72,10 @@ cudaError_t launch_merge(const float* dist, const int32_t* ids, int32_t n_lists,
                          float* out_dist, int32_t* out_ids, cudaStream_t s);
 size_t search_smem_bytes(const IndexView& ix, const SearchCfg& c, int warps_per_block);
 cudaError_t plan_search(const IndexView& ix, const SearchCfg& c, int64_t nq, int warps_per_block, int* wpq);
+cudaError_t launch_peer_signal(unsigned long long* const* flags, int n_peers, int slot, unsigned long long value,
+                               cudaStream_t s);
+cudaError_t launch_peer_wait(const unsigned long long* flags, int n, unsigned long long value,
+                             unsigned long long timeout_ns, int32_t* status, cudaStream_t s);
 cudaError_t launch_build_inline(const IndexView& ix, uint8_t* blk, cudaStream_t s);
 cudaError_t launch_code_norms(const IndexView& ix, int32_t* out, cudaStream_t s);
 // GPU index build (build.cu): codes [n x d_pad32] (d_pad32 a multiple of 32, zero padded), their

@@ -121,6 +121,22 @@ namespace {
 #define AQR_FLAT_MERGE 10  // > 0: the W insert takes one chunked pass when np * this > entries moved (0: off;
                           // 10: C5 2.98 -> 2.86 ms, C2 9.64 -> 9.60; 40: C2 9.92)
 #endif
+#ifndef AQR_PF_PASSES
+#define AQR_PF_PASSES 0  // 1: before the first gather pass of an expansion, the code rows of the later
+                         // passes are prefetched into L2 (prefetch.global.L2: no registers, no result)
+#endif
+#ifndef AQR_PF_ROW
+#define AQR_PF_ROW 0  // 1: the scan for the first unexpanded W entry after the pick runs before the scoring, and
+                      // that node's adjacency row (the next expansion unless a smaller new key arrives) is
+                      // prefetched into L2
+#endif
+#ifndef AQR_PF_FINISH
+#define AQR_PF_FINISH 0  // 1: Stage 2's code rows and Stage 3's fp32 rows are prefetched into L2 before their
+                         // 4-row loops (each loop step is otherwise one exposed round trip)
+#endif
+#ifndef AQR_CMIN_GUARD
+#define AQR_CMIN_GUARD 0  // 1: the warp-wide minimum of the new keys is skipped when the expansion has none
+#endif
 #ifndef AQR_FUSED_FILTER
 #define AQR_FUSED_FILTER 1  // 1: layer-0 scoring and the max-W filter in one pass (list_filter)
 #endif
@@ -617,6 +633,21 @@ __device__ __forceinline__ int list_filter(const IndexView& ix, const C32 (&qreg
   // warp; a fixed row would put every warp's absent rows on one L2 line -- measured, a hot spot)
   const int alt = max(ids[0], 0);
   int np0 = 0;
+#if AQR_PF_PASSES
+  // a pass waits for the slowest of its G * U rows (some row misses L2 in nearly every pass): the
+  // rows of passes 2.. are requested now, so those passes find them in L2
+  for (int i = G * U + lane; i < m; i += 32) {
+    const int id = ids[i];
+    if (id >= 0) {
+      // every 128-byte line the row touches (rows of d_pad = 96 straddle lines)
+      const uint64_t a0 = reinterpret_cast<uint64_t>(ix.codes) + (uint64_t)(uint32_t)id * dpad;
+      for (uint64_t a = a0 & ~127ull; a < a0 + dpad; a += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+#if AQR_PF_PASSES >= 2
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(ix.xnorm + id));
+#endif
+    }
+  }
+#endif
   for (int r0 = 0; r0 < m; r0 += G * U) {
     const int32_t* idp = ids + r0 + g * U;
     // |x^|^2 of the rows whose totals this lane holds after the reduction
@@ -968,6 +999,12 @@ __device__ __forceinline__ float div_code(float a, float s, float r) {
   return __fmaf_rn(__fmaf_rn(-q0, s, a), r, q0);
 }
 
+// every 128-byte line of [p, p + bytes) requested into L2 (no register result)
+__device__ __forceinline__ void prefetch_l2_range(const void* p, uint32_t bytes) {
+  const uint64_t a0 = reinterpret_cast<uint64_t>(p);
+  for (uint64_t a = a0 & ~127ull; a < a0 + bytes; a += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
+
 // four rows at once (rows with id < 0 give 0), their loads in flight together.  Per row: lanes own
 // 4-wide chunks c = lane + 32 t, one FMA per term in increasing c, then a butterfly sum.
 // Stage 2 (EXACT = false) decodes the codes x~ = x^ / scale + min (IEEE division, Alg2 l.11);
@@ -1072,6 +1109,12 @@ void finish_query(const IndexView& ix, const SearchCfg& c, const float* qf, cons
                              int32_t* out_ids, float* out_dist, const aqr_debug& dbg, bool has_dbg, int lane,
                              int32_t* cnt) {
   // Stage 2: d^a for every entry of C (Alg2 l.10-12)
+  if (AQR_PF_FINISH) {
+    for (int i = lane; i < nc; i += 32) {
+      const int32_t id = cid ? cid[i] : qkey_id(wk[i]);
+      prefetch_l2_range(ix.codes + (int64_t)id * ix.d_pad, (uint32_t)ix.d_pad);
+    }
+  }
   for (int i0 = 0; i0 < nc; i0 += 4) {
     int32_t id[4];
 #pragma unroll
@@ -1104,6 +1147,10 @@ void finish_query(const IndexView& ix, const SearchCfg& c, const float* qf, cons
   if (AQR_ADAPTIVE && !isinf(c.tau_spread) && nc > 0) depth = adaptive_depth(akeys, nc, k, c.tau_spread, depth, lane);
   if (term && depth > k) depth = k;
   // Stage 3: exact distances for A[0:depth] (Alg2 l.19-22)
+  if (AQR_PF_FINISH) {
+    for (int i = lane; i < depth; i += 32)
+      prefetch_l2_range(ix.base + (int64_t)(int32_t)(uint32_t)akeys[i] * ix.d4, 4u * (uint32_t)ix.d4);
+  }
   for (int i0 = 0; i0 < depth; i0 += 4) {
     int32_t id[4];
 #pragma unroll
@@ -1439,6 +1486,28 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
         if (has_dbg && dbg.exp_ids && nexp < dbg.exp_cap) dbg.exp_ids[qi * dbg.exp_cap + nexp] = cnode;
       }
       ++nexp;
+      uint64_t kw_e = ~0ull;
+      int kwpos_e = -1;
+      if (AQR_PF_ROW && !INL && !HINT) {
+        // W does not change until the merge: find the next unexpanded entry now and pull its
+        // adjacency row into L2 (no registers held); ~half of the expansions insert nothing, and
+        // then this row's load would be fully exposed
+        for (int bb = pos + 1; bb < size; bb += 32) {
+          const int i = bb + lane;
+          const bool un = i < size && !(W[i] & 1ull);
+          const uint32_t mk = __ballot_sync(kFull, un);
+          if (mk) {
+            kwpos_e = bb + __ffs(mk) - 1;
+            kw_e = W[kwpos_e];
+            break;
+          }
+        }
+        if (kwpos_e >= 0) {
+          const uint64_t a0 = reinterpret_cast<uint64_t>(ix.adj0 + (int64_t)qkey_id(kw_e) * ix.ld0);
+          const uint64_t a = (a0 & ~127ull) + 128ull * lane;
+          if (a < a0 + 4ull * ix.cap0) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+        }
+      }
       int m;
       const int32_t* ids;
       if (INL) {
@@ -1583,7 +1652,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
         // the next expansion is min(first unexpanded entry of W after pos, smallest candidate);
         // start loading its layer-0 data now so the load overlaps the merge (prefetch only,
         // never speculative: this node IS expanded next)
-        cmin = warp_min_u64(cmin);
+        if (!AQR_CMIN_GUARD || np > 0) cmin = warp_min_u64(cmin);  // np == 0: every lane holds ~0
         uint64_t kw = ~0ull;
         int kwpos = -1;
         if (HINT && khint != -1) {
@@ -1591,6 +1660,9 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
             kwpos = khint;
             kw = W[khint];
           }
+        } else if (AQR_PF_ROW && !INL && !HINT) {
+          kwpos = kwpos_e;
+          kw = kw_e;
         } else
         for (int bb = pos + 1; bb < size; bb += 32) {
           const int i = bb + lane;
