@@ -707,8 +707,8 @@ def run_aqr(args):
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "frac_pipelined": round(bytes_launch / (ms_per_step / 1e3) / 1e9 / peak, 4),
                          "limiter": ("below the HBM roofline the kernel is bound by per-warp dependent chains and "
-                                     "issue (ncu: DRAM ~11% of peak, L2 hit ~78%, issue ~62% busy; "
-                                     "profiles/r02/ncu_search_c2_head*.txt)"),
+                                     "issue (ncu: DRAM ~11% of peak, L2 hit ~78%, issue ~59% busy; "
+                                     "profiles/r02/ncu_search_c2_s4final*.txt)"),
                          "bytes_per_query": round(bq, 1), "sector_bytes_per_query": round(bq_sector, 1),
                          "peak_source": peak_src,
                          "distinct_eval_ratio": round(ratio, 4), "distinct_ratio_sample": n_ratio,
