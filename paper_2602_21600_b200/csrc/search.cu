@@ -887,11 +887,15 @@ __device__ __forceinline__ bool visit_new(uint32_t* h, int hbits, int32_t u, int
 // on [0, 2^B); its top hbits bits pick the slot and the low htag (<= 15) bits are stored, so (slot,
 // tag) identifies u exactly -- a hit is never a false positive -- at half the bytes of an id slot
 // (twice the slots in the same shared memory).  Empty slots hold 0xFFFF (no tag reaches 2^15)
+// TW: the set-associative forms below (AQR_HASH_2WAY) are compiled only into the wide-row
+// instantiations (CAP > 56: the configs that use the table, C1 / C5); compiled into the CAP 56
+// kernel too, the unused code cost C2 0.4% (9.647 vs 9.605 ms, 3 x 6 runs each)
+template <bool TW>
 __device__ __forceinline__ bool visit_new16(uint16_t* h, const SearchCfg& c, int32_t u) {
   const uint32_t x = ((uint32_t)u * c.hmul) & c.hmaskb;
 #if AQR_HASH_2WAY == 2
   // four-way sets (one 64-bit word, tags in LRU order from the low half of .x), tag = htag + 2 bits
-  if (c.htag < 14) {
+  if (TW && c.htag < 14) {
     uint2* h64 = reinterpret_cast<uint2*>(h) + (x >> (c.htag + 2));
     const uint32_t t = x & ((4u << c.htag) - 1u);
     const uint2 w = *h64;
@@ -909,7 +913,7 @@ __device__ __forceinline__ bool visit_new16(uint16_t* h, const SearchCfg& c, int
   // bit that no longer indexes joins the tag (htag + 1 <= 15 bits, so 0xFFFF stays "empty").  A hit
   // on the older way moves it to the front; a miss evicts the older way.  Lanes that race on one
   // set lose an insertion at worst (a later re-evaluation), never invent a tag
-  if (c.htag < 15) {
+  if (TW && c.htag < 15) {
     uint32_t* h32 = reinterpret_cast<uint32_t*>(h) + (x >> (c.htag + 1));
     const uint32_t t = x & ((2u << c.htag) - 1u);
     const uint32_t w = *h32;
@@ -1440,7 +1444,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
       if (lane == 0) {
         W[0] = qkey(dcur, cur);
         if (vhash) {
-          if (c.htag >= 0) visit_new16(reinterpret_cast<uint16_t*>(hash), c, cur);
+          if (c.htag >= 0) visit_new16<(AQR_HASH_2WAY > 0 && CAP > 56)>(reinterpret_cast<uint16_t*>(hash), c, cur);
           else visit_new(hash, c.hbits, cur, fails);
         }
         if (vbm) atomicOr(vbm + (cur >> 5), 1u << (cur & 31));
@@ -1618,7 +1622,7 @@ __global__ void __launch_bounds__(32 * AQR_WARPS_PER_CTA, (LPR == 32 && AQR_WIDE
             deg += __popc(__ballot_sync(kFull, u >= 0));
             bool keep = u >= 0;
             if (keep && vhash)
-              keep = c.htag >= 0 ? visit_new16(reinterpret_cast<uint16_t*>(hash), c, u) : visit_new(hash, c.hbits, u, fails);
+              keep = c.htag >= 0 ? visit_new16<(AQR_HASH_2WAY > 0 && CAP > 56)>(reinterpret_cast<uint16_t*>(hash), c, u) : visit_new(hash, c.hbits, u, fails);
             const uint32_t mk = __ballot_sync(kFull, keep);
             AQR_ASSERT(!keep || m + __popc(mk & ((1u << lane) - 1u)) < H::NB);
             if (keep) nb[m + __popc(mk & ((1u << lane) - 1u))] = u;
@@ -2185,7 +2189,7 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
         sm->np[0] = sm->np[1] = 0;
         sm->cmin[0] = sm->cmin[1] = ~0ull;
         if (vhash) {
-          if (c.htag >= 0) visit_new16(reinterpret_cast<uint16_t*>(vhash), c, cur);
+          if (c.htag >= 0) visit_new16<(AQR_HASH_2WAY > 0 && CAP > 56)>(reinterpret_cast<uint16_t*>(vhash), c, cur);
           else visit_new(vhash, c.hbits, cur, fails);
         }
         if (vbm) atomicOr(vbm + (cur >> 5), 1u << (cur & 31));
@@ -2264,7 +2268,7 @@ __global__ void __launch_bounds__(32 * G, AQR_COOP_MIN_CTAS) coop_kernel(IndexVi
             keep[r] = u >= 0 && !(old[r] & (1u << (u & 31)));
             if (AQR_VBM_LOAD && keep[r]) vbm_set(vbm + (u >> 5), 1u << (u & 31), vpol);
           }
-          else keep[r] = u >= 0 && (c.htag >= 0 ? visit_new16(reinterpret_cast<uint16_t*>(vhash), c, u)
+          else keep[r] = u >= 0 && (c.htag >= 0 ? visit_new16<(AQR_HASH_2WAY > 0 && CAP > 56)>(reinterpret_cast<uint16_t*>(vhash), c, u)
                                                 : visit_new(vhash, c.hbits, u, fails));
           const uint32_t mk = __ballot_sync(kFull, keep[r]);
           if (lane == 0) sm->wcnt[r * G + w] = __popc(mk);
