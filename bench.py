@@ -720,6 +720,7 @@ def run_aqr(args):
             "gpu_launches": args.steps,
             "ms_per_step_isolated": round(launch_ms, 4),
             "steady_state": steady,
+            "lib": aqr.lib().aqr_version().decode(),  # "... src:<hash of the CUDA sources libaqr.so was built from>"
             "clocks": clk,
             "ef_sweep": sweep,
             "counters_per_query": {n: round(float(v) / len(q), 2) for n, v in zip(aqr.COUNTER_NAMES, tot_counters)},
@@ -1048,6 +1049,7 @@ def run_sharded(args):
                     "d2h_bytes_per_step": int(nq * k * 8)},
             "gpu_launches": args.steps * ((len(shards) + (1 if len(shards) > 1 else 0) + (1 if world > 1 else 0)) if ex is None
                                           else (len(shards) * sum(1 for lo_, hi_ in blocks if hi_ > lo_) + 3)),
+            "lib": aqr.lib().aqr_version().decode(),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
